@@ -1,0 +1,125 @@
+/*
+ * nmfa_b200.h -- C ABI of the B200-native noisy mean-field annealing sampler.
+ *
+ * The reference package (`nmfa`, pure Python) has no native FFI; its operator
+ * boundary is the per-run kernel pair bound in kernels.py:30-31 and its
+ * sampling entry point is nmfa_batch (solver.py:262-280).  This header is the
+ * native boundary the Python mirror in `paper_1806_08422_b200` binds through
+ * ctypes (see INTEGRATION.md for the binding a maintainer of the reference
+ * would add).  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *  - Every function returns 0 on success and a nonzero NMFA_ERR_* code on
+ *    failure; nmfa_last_error() then holds a thread-local message.  Argument
+ *    errors mirror the reference's ValueError messages (solver.py:196-205,
+ *    problem.py:25-62); CUDA failures return NMFA_ERR_CUDA.
+ *  - "dev" pointers are CUDA device pointers on the problem's device; "host"
+ *    pointers are ordinary host memory.  `stream` is a cudaStream_t (NULL =
+ *    legacy default stream).  Device entry points are asynchronous.
+ *  - Replica r of a call with first global index r0 uses noise key seed+r0+r,
+ *    so results do not depend on how replicas are split over calls or GPUs.
+ */
+#ifndef NMFA_B200_H_
+#define NMFA_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMFA_OK 0
+#define NMFA_ERR_ARG 1   /* invalid argument (reference: ValueError) */
+#define NMFA_ERR_CUDA 2  /* CUDA runtime / launch failure (RuntimeError) */
+#define NMFA_ERR_STATE 3 /* wrong object state / unsupported request */
+
+/* Kernel path chosen for a problem (internal detail, reported for tests). */
+#define NMFA_PATH_SMALL 0  /* n <= 256: persistent tcgen05 kernel, J in SMEM */
+#define NMFA_PATH_DENSE 1  /* dense n > 256: tcgen05 GEMM step, J streamed */
+#define NMFA_PATH_SPARSE 2 /* sparse n > 256: CSR gather step */
+
+typedef struct nmfa_problem nmfa_problem_t;
+typedef struct nmfa_plan nmfa_plan_t;
+
+typedef struct {
+  int64_t n;
+  int64_t n_edges;
+  double density;      /* edges / (n(n-1)/2), problem.py:96-99 */
+  int32_t is_dense;    /* density > 0.5, the reference's dispatch bit */
+  int32_t path;        /* NMFA_PATH_* */
+  int32_t j_exact;     /* 1 if every coupler is exact in the fp16 operand */
+  int32_t int_weights; /* 1 if all weights and fields are integers */
+  double j_scale;      /* power-of-two scale applied to J on device */
+} nmfa_problem_info_t;
+
+/* Build an immutable device-resident problem from the canonical coupler
+ * list (IsingProblem(n, couplers, h), problem.py:25-116).  Edges may come in
+ * any order and orientation; they are canonicalised to i<j.  Validation and
+ * error text follow problem.py:25-62.  h_host may be NULL (zero fields).
+ * Replaces: IsingProblem construction + the dense/CSR arrays handed to
+ * kernels.anneal_dense / kernels.anneal_sparse (solver.py:206-216). */
+int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* edges_i_host,
+                        const int64_t* edges_j_host, const double* weights_host,
+                        const double* h_host, int32_t device, nmfa_problem_t** out);
+int nmfa_problem_destroy(nmfa_problem_t* p);
+int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info);
+/* Force a kernel path (tests / crossover studies); NMFA_ERR_ARG if the path
+ * cannot run this problem (e.g. SMALL with n > 256). */
+int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path);
+
+/* A plan owns the device state for `n_reads` replicas and `t_f` steps so
+ * repeated runs allocate nothing and can be captured in a CUDA graph.
+ * temps_host: t_f temperatures (Schedule.temperatures, solver.py:70-84),
+ * each > 0.  alpha in [0,1], sigma >= 0 (NmfaParams, solver.py:141-162). */
+int nmfa_plan_create(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,
+                     const double* temps_host, double alpha, double sigma,
+                     nmfa_plan_t** out);
+int nmfa_plan_destroy(nmfa_plan_t* plan);
+
+/* Run one batch of `n_reads` anneals from the plan.  Replaces
+ * nmfa_batch (solver.py:262-280) / _run (236-253) for all replicas at once.
+ *   noise_dev   [n_reads][t_f][n] f32 pre-scaled additive noise, or NULL to
+ *               draw in-kernel Philox noise (run_with_noise seam, 188-218)
+ *   s0_dev      [n_reads][n] f32 initial analog spins, or NULL for zeros
+ *   config_dev  [n_reads][n] i8 out: sign_round(s) in {-1,+1} (181-183)
+ *   energy_dev  [n_reads] f64 out: energy(config) (150-154), or NULL
+ *   s_final_dev [n_reads][n] f32 out, or NULL
+ *   s_hist_dev  [n_reads][t_f][n] f32 out (record_trajectory), or NULL
+ *   e_hist_dev  [n_reads][t_f] f64 out, requires s_hist_dev, or NULL */
+int nmfa_plan_run(nmfa_plan_t* plan, uint64_t seed, int64_t r0, const float* noise_dev,
+                  const float* s0_dev, int8_t* config_dev, double* energy_dev,
+                  float* s_final_dev, float* s_hist_dev, double* e_hist_dev, void* stream);
+
+/* One-shot convenience over plan_create/plan_run/plan_destroy. */
+int nmfa_anneal(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,
+                const double* temps_host, double alpha, double sigma, uint64_t seed,
+                int64_t r0, const float* noise_dev, const float* s0_dev, int8_t* config_dev,
+                double* energy_dev, float* s_final_dev, float* s_hist_dev,
+                double* e_hist_dev, void* stream);
+
+/* Same batch with HOST buffers (H2D of inputs, D2H of results inside the
+ * call; synchronous).  This is the end-to-end entry a non-CUDA host binds. */
+int nmfa_anneal_host(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,
+                     const double* temps_host, double alpha, double sigma, uint64_t seed,
+                     int64_t r0, int8_t* config_host, double* energy_host);
+
+/* energy(problem, config) for a batch of +-1 configs (problem.py:150-154).
+ * Bit-exact for integer weights/fields (f64 accumulation of integers),
+ * within ~1e-15 relative otherwise. */
+int nmfa_energy(const nmfa_problem_t* p, const int8_t* config_dev, int64_t n_configs,
+                double* energy_dev, void* stream);
+
+/* best-of-reads: minimum energy and the lowest index attaining it
+ * (cli.py:236 min; metrics.py:105). */
+int nmfa_best_of(const double* energy_dev, int64_t n, double* best_energy_dev,
+                 int64_t* best_index_dev, void* stream);
+
+const char* nmfa_last_error(void);
+const char* nmfa_version(void);
+/* Number of kernels the last nmfa_plan_run on this thread enqueued. */
+int64_t nmfa_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMFA_B200_H_ */

@@ -1,0 +1,255 @@
+"""CPU oracle for the NMFA hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a float64 numpy restatement of the reference package `nmfa`
+(King et al., arXiv 1806.08422, Algorithm 1).  It exists to check the CUDA
+path, never to replace it: only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import it.  The
+product package `paper_1806_08422_b200` never imports anything from here and
+fails loudly when its CUDA library is missing.
+
+Parity pinning: every function below is checked in `tests/test_oracle.py`
+against golden vectors produced by running the reference itself in the
+build container (`tests/golden/make_golden.py`, committed with its outputs).
+
+Third-party arithmetic restated (the reference leaves versions unpinned,
+pyproject.toml:10-14): numpy's Philox4x64-10 bit generator + ziggurat
+`standard_normal` (solver.py:182-185, 238-241) -- used here through numpy
+itself, since the stream identity *is* numpy's; BLAS dgemv/dgemm via `@`.
+"""
+
+from __future__ import annotations
+
+import math
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+RUN_STREAM_TAG = 2          # solver.py:33
+GEN_STREAM_TAG = 1          # generators.py:13
+DEFAULT_BREAKPOINTS = ((0.0, 2.0), (0.25, 0.8), (0.75, 0.2), (1.0, 0.02))  # solver.py:133
+DENSE_THRESHOLD = 0.5       # problem.py:13
+TIE_TOL = 1e-9              # metrics.py:21
+
+
+# --------------------------------------------------------------------------
+# schedule (solver.py:70-84)
+# --------------------------------------------------------------------------
+def temperatures(t_f, breakpoints=DEFAULT_BREAKPOINTS):
+    """Piecewise-geometric T for iterations 1..t_f (solver.py:70-84)."""
+    fs = np.array([float(f) for f, _ in breakpoints])
+    Ts = np.array([float(T) for _, T in breakpoints])
+    t_f = int(t_f)
+    f = np.zeros(1) if t_f == 1 else np.arange(t_f) / (t_f - 1)
+    k = np.clip(np.searchsorted(fs, f, side="right") - 1, 0, len(fs) - 2)
+    frac = (f - fs[k]) / (fs[k + 1] - fs[k])
+    out = Ts[k] * (Ts[k + 1] / Ts[k]) ** frac
+    out[f >= fs[-1]] = Ts[-1]
+    return out
+
+
+# --------------------------------------------------------------------------
+# randomness (solver.py:182-185, 236-241)
+# --------------------------------------------------------------------------
+def noise_stream(seed):
+    """numpy Philox4x64-10 keyed (2 << 64) | seed (solver.py:182-185)."""
+    key = (RUN_STREAM_TAG << 64) | (int(seed) & MASK64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def run_noise(seed, t_f, n, sigma):
+    """Pre-scaled additive noise of one run, shape (t_f, n) (solver.py:238-241)."""
+    z = noise_stream(seed).standard_normal((int(t_f), int(n)))
+    if sigma != 1.0:
+        z *= sigma
+    return z
+
+
+# --------------------------------------------------------------------------
+# problem arithmetic (problem.py:25-116, 150-183)
+# --------------------------------------------------------------------------
+class Problem:
+    """Canonical edge list + symmetric CSR + normalizers (problem.py:25-116)."""
+
+    def __init__(self, n, couplers=(), h=None):
+        self.n = n = int(n)
+        self.h = np.zeros(n) if h is None else np.asarray(h, dtype=np.float64).copy()
+        arr = np.asarray(couplers, dtype=np.float64).reshape(-1, 3)
+        ii = arr[:, 0].astype(np.int64)
+        jj = arr[:, 1].astype(np.int64)
+        ww = arr[:, 2].copy()
+        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+        order = np.lexsort((hi, lo))                       # problem.py:63-66
+        self.edges_i, self.edges_j, self.edge_weights = lo[order], hi[order], ww[order]
+        rows = np.concatenate([self.edges_i, self.edges_j])  # problem.py:78-88
+        cols = np.concatenate([self.edges_j, self.edges_i])
+        vals = np.concatenate([self.edge_weights, self.edge_weights])
+        perm = np.lexsort((cols, rows))
+        self.csr_indptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows, minlength=n), out=self.csr_indptr[1:])
+        self.csr_indices = cols[perm]
+        self.csr_weights = vals[perm]
+        norm = np.sqrt(self.h ** 2 + np.bincount(rows, weights=vals ** 2, minlength=n))
+        self.normalizers_safe = np.where(norm == 0.0, 1.0, norm)   # problem.py:90-95
+        pairs = n * (n - 1) // 2
+        self.density = 0.0 if pairs == 0 else self.edges_i.size / pairs
+        self.is_dense = self.density > DENSE_THRESHOLD              # problem.py:97-99
+        J = np.zeros((n, n))
+        J[self.edges_i, self.edges_j] = self.edge_weights
+        J[self.edges_j, self.edges_i] = self.edge_weights
+        self.dense = J
+
+
+def sign_round(s):
+    """s < 0 -> -1, else +1 (0 and -0 -> +1) (problem.py:181-183)."""
+    return np.where(np.asarray(s, dtype=np.float64) < 0.0, -1.0, 1.0)
+
+
+def energy(p, config):
+    """sum_(i<j) w c_i c_j + h.c over the canonical edge list (problem.py:150-154)."""
+    c = np.asarray(config, dtype=np.float64)
+    pair = float(np.dot(p.edge_weights, c[p.edges_i] * c[p.edges_j]))
+    return pair + float(np.dot(p.h, c))
+
+
+def energies(p, configs):
+    """Row-wise `energy` for a (R, n) batch of +-1 configurations."""
+    C = np.asarray(configs, dtype=np.float64)
+    return (C[:, p.edges_i] * C[:, p.edges_j]) @ p.edge_weights + C @ p.h
+
+
+def cut_value(p, config):
+    """sum w (1 - c_i c_j) / 2 (problem.py:157-163)."""
+    c = np.asarray(config, dtype=np.float64)
+    return float(np.dot(p.edge_weights, 1.0 - c[p.edges_i] * c[p.edges_j])) * 0.5
+
+
+# --------------------------------------------------------------------------
+# the anneal loop (_kernels_numpy.py:17-53 / _kernels_numba.py:39-80)
+# --------------------------------------------------------------------------
+def anneal(p, s, temps, noise, alpha, record=False):
+    """One run: s <- a*(-tanh(((h + J s)/norm + noise_t)/T_t)) + (1-a)*s per step.
+
+    Dense problems use the BLAS matvec (_kernels_numba.py:72-75); sparse ones
+    the CSR row sum in column order (_kernels_numba.py:48-56).  Returns
+    (s, s_hist, e_hist) like the reference kernels.
+    """
+    s = np.array(s, dtype=np.float64)
+    t_f = len(temps)
+    s_hist = np.empty((t_f if record else 0, p.n))
+    e_hist = np.empty(t_f if record else 0)
+    if p.is_dense:
+        mv_of = lambda v: np.dot(p.dense, v)
+    else:
+        import scipy.sparse as sp
+        csr = sp.csr_matrix((p.csr_weights, p.csr_indices, p.csr_indptr), shape=(p.n, p.n))
+        mv_of = lambda v: csr @ v
+    for t in range(t_f):
+        phi = (p.h + mv_of(s)) / p.normalizers_safe + noise[t]
+        s = alpha * (-np.tanh(phi / temps[t])) + (1.0 - alpha) * s
+        if record:
+            s_hist[t] = s
+            e_hist[t] = energy(p, sign_round(s))
+    return s, s_hist, e_hist
+
+
+def run(p, seed, t_f=1000, alpha=0.15, sigma=0.15, temps=None):
+    """One seeded run (solver.py:236-253): returns (config, energy)."""
+    temps = temperatures(t_f) if temps is None else temps
+    s, _, _ = anneal(p, np.zeros(p.n), temps, run_noise(seed, t_f, p.n, sigma), alpha)
+    cfg = sign_round(s)
+    return cfg, energy(p, cfg)
+
+
+def batch(p, seed, n_runs, t_f=1000, alpha=0.15, sigma=0.15, threads=1):
+    """n_runs independent runs, run k seeded seed+k (solver.py:262-280)."""
+    temps = temperatures(t_f)
+    seeds = [(int(seed) + k) & MASK64 for k in range(int(n_runs))]
+    one = lambda sd: run(p, sd, t_f, alpha, sigma, temps)
+    if threads <= 1:
+        out = [one(sd) for sd in seeds]
+    else:
+        with ThreadPoolExecutor(max_workers=int(threads)) as pool:
+            out = list(pool.map(one, seeds))
+    return np.array([c for c, _ in out]), np.array([e for _, e in out])
+
+
+def batched_anneal(p, seeds, t_f=1000, alpha=0.15, sigma=0.15, temps=None, noise=None):
+    """Replica-batched float64 restatement: S is (n, R), one GEMM per step.
+
+    Replica r draws its per-step noise from noise_stream(seeds[r]) in the same
+    order as the reference's (t_f, n) matrix (test_solver.py:181-190 pins
+    that per-step draws equal the one-shot draw).  When `noise` (R, t_f, n) is
+    given it is used instead.  Returns final analog S as (R, n).
+    """
+    temps = temperatures(t_f) if temps is None else np.asarray(temps, dtype=np.float64)
+    R = len(seeds) if noise is None else noise.shape[0]
+    S = np.zeros((p.n, R))
+    gens = None if noise is not None else [noise_stream(sd) for sd in seeds]
+    J = p.dense
+    hn = p.h[:, None]
+    nrm = p.normalizers_safe[:, None]
+    for t in range(len(temps)):
+        if noise is None:
+            Z = np.stack([g.standard_normal(p.n) for g in gens], axis=1)
+            if sigma != 1.0:
+                Z *= sigma
+        else:
+            Z = noise[:, t, :].T
+        phi = (hn + J @ S) / nrm + Z
+        S = alpha * (-np.tanh(phi / temps[t])) + (1.0 - alpha) * S
+    return S.T.copy()
+
+
+# --------------------------------------------------------------------------
+# benchmark statistics (metrics.py:70-94)
+# --------------------------------------------------------------------------
+def success_probability(final_energies, e_ref):
+    e = np.asarray(final_energies, dtype=np.float64)
+    return float(np.count_nonzero(e <= e_ref + TIE_TOL)) / e.size
+
+
+def time_to_solution(p, tau, confidence=0.99):
+    if p == 0.0:
+        return math.inf
+    if p >= confidence:
+        return tau
+    return tau * math.log(1.0 - confidence) / math.log(1.0 - p)
+
+
+def wilson_interval(k, n, z=1.96):
+    """Wilson score interval for a binomial proportion."""
+    if n == 0:
+        return (0.0, 1.0)
+    ph = k / n
+    den = 1.0 + z * z / n
+    c = (ph + z * z / (2 * n)) / den
+    half = z * math.sqrt(ph * (1 - ph) / n + z * z / (4 * n * n)) / den
+    return (c - half, c + half)
+
+
+# --------------------------------------------------------------------------
+# instance generators (generators.py:16-86) -- used to pin the package's
+# own generators against golden fixtures
+# --------------------------------------------------------------------------
+def _gen_rng(seed):
+    return np.random.Generator(np.random.Philox(key=(GEN_STREAM_TAG << 64) | (int(seed) & MASK64)))
+
+
+def gen_sk_edges(n, seed):
+    ii, jj = np.triu_indices(int(n), 1)
+    w = np.where(_gen_rng(seed).random(ii.size) < 0.5, 1.0, -1.0)
+    return ii.astype(np.int64), jj.astype(np.int64), w
+
+
+def moebius_edges(n):
+    cyc_i = np.arange(n, dtype=np.int64)
+    cyc_j = (cyc_i + 1) % n
+    half = np.arange(n // 2, dtype=np.int64)
+    ii = np.concatenate([np.minimum(cyc_i, cyc_j), half])
+    jj = np.concatenate([np.maximum(cyc_i, cyc_j), half + n // 2])
+    return ii, jj, np.ones(ii.size)
+
+
+def problem_from_edges(n, ii, jj, w, h=None):
+    return Problem(n, np.column_stack([ii, jj, w]), h)

@@ -1,0 +1,215 @@
+// Persistent small-N NMFA kernel (n <= 256, any density): the whole anneal in
+// one launch.  One CTA owns 128 replicas for all t_f steps:
+//   J (B operand, fp16, K-major)      -> SMEM, loaded once
+//   S (A operand, fp16, K-major)      -> SMEM, rewritten by the epilogue
+//   Phi accumulator  D = S J^T        -> TMEM columns [0, np)
+//   fp32 master S                     -> TMEM columns [np, 2np)
+// Per step: one thread issues np/16 tcgen05.mma (M=128, N=np, K=16), commits
+// to an mbarrier; every warp then drains its TMEM lane quarter, applies the
+// fused update (reference _kernels_numba.py:71-75) and writes the new fp16
+// operand back into SMEM.  No HBM traffic inside the anneal.
+#include "common.cuh"
+#include "internal.h"
+
+namespace nmfa {
+
+struct SmallArgs {
+  const uint4* j_img;
+  uint32_t j_bytes;
+  const float* invn;
+  const float* hn;
+  const float* inv_temp;
+  int n, np, t_f;
+  uint32_t tmem_cols;
+  float alpha, oma, sigma;
+  unsigned long long key_base;
+  long long R;
+  const float* noise;  // [R][t_f][n] or null
+  const float* s0;     // [R][n] or null
+  int8_t* cfg;         // [R][n]
+  float* s_out;        // [R][n] or null
+  float* s_hist;       // [R][t_f][n] or null
+  int cs;              // warps per TMEM lane quarter (column split)
+};
+
+constexpr uint32_t kRowsPerCta = 128;
+constexpr uint32_t kLboA = (kRowsPerCta / 8) * 128;  // A: K core matrices 2048 B apart
+
+__global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int np = a.np;
+  uint8_t* sJ = smem;
+  uint8_t* sA = smem + (size_t)np * np * 2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kRowsPerCta * np * 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, cpart = warp >> 2;
+  const int rl = 32 * quarter + lane;
+  const long long rrel = (long long)blockIdx.x * kRowsPerCta + rl;
+  const bool valid = rrel < a.R;
+  const int nchunks = np / 16;
+
+  for (uint32_t i = tid; i < a.j_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sJ)[i] = a.j_img[i];
+  if (warp == 0) tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t t_acc = tbase + ((uint32_t)(32 * quarter) << 16);
+  const uint32_t t_mst = t_acc + (uint32_t)np;
+
+  const unsigned long long key = a.key_base + (unsigned long long)rrel;
+  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+
+  // initial state: s0 or zeros, into the TMEM master and the SMEM operand
+  for (int j = cpart; j < nchunks; j += a.cs) {
+    const int c0 = 16 * j;
+    float v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      int i = c0 + c;
+      v[c] = (a.s0 && valid && i < a.n) ? a.s0[rrel * a.n + i] : 0.f;
+    }
+    tmem_st16(t_mst + c0, v);
+    uint4 lo = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+                          pack_half2(v[6], v[7]));
+    uint4 hi = make_uint4(pack_half2(v[8], v[9]), pack_half2(v[10], v[11]),
+                          pack_half2(v[12], v[13]), pack_half2(v[14], v[15]));
+    *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0, kLboA)) = lo;
+    *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8, kLboA)) = hi;
+  }
+  tmem_wait_st();
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+
+  const uint32_t idesc = make_idesc_f16(kRowsPerCta, (uint32_t)np);
+  const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sJ);
+  const uint32_t lboB = (uint32_t)np * 16u;
+
+  for (int t = 0; t < a.t_f; ++t) {
+    if (tid == 0) {
+      tc_fence_after();
+      for (int ks = 0; ks < nchunks; ++ks) {
+        uint64_t ad = make_desc_noswizzle(a_addr + ks * 2 * kLboA, kLboA, 128);
+        uint64_t bd = make_desc_noswizzle(b_addr + ks * 2 * lboB, lboB, 128);
+        mma_f16_ss(tbase, ad, bd, idesc, ks > 0 ? 1u : 0u);
+      }
+      mma_commit(bar);
+    }
+    mbar_wait(bar, (uint32_t)(t & 1));
+    tc_fence_after();
+    const float inv_t = a.inv_temp[t];
+    const bool last = (t == a.t_f - 1);
+
+    for (int j = cpart; j < nchunks; j += a.cs) {
+      const int c0 = 16 * j;
+      float acc[16], ms[16], z[16];
+      tmem_ld16(t_acc + c0, acc);
+      tmem_ld16(t_mst + c0, ms);
+      tmem_wait_ld();
+      if (a.noise) {
+        const float* nz = a.noise + ((long long)rrel * a.t_f + t) * a.n;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) z[c] = (valid && c0 + c < a.n) ? nz[c0 + c] : 0.f;
+      } else {
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) normal4(k0, k1, (uint32_t)(c0 / 4 + qq), (uint32_t)t, &z[4 * qq]);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) z[c] *= a.sigma;
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int i = c0 + c;
+        ms[c] = (i < a.n) ? nmfa_update(acc[c], a.invn[i], a.hn[i], z[c], inv_t, a.alpha, a.oma, ms[c])
+                          : 0.f;
+      }
+      tmem_st16(t_mst + c0, ms);
+      uint4 lo = make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
+                            pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
+      uint4 hi = make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
+                            pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
+      *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0, kLboA)) = lo;
+      *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8, kLboA)) = hi;
+      if (valid) {
+        if (a.s_hist) {
+          float* hrow = a.s_hist + ((long long)rrel * a.t_f + t) * a.n;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c0 + c < a.n) hrow[c0 + c] = ms[c];
+        }
+        if (last) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int i = c0 + c;
+            if (i < a.n) {
+              a.cfg[rrel * a.n + i] = ms[c] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181-183
+              if (a.s_out) a.s_out[rrel * a.n + i] = ms[c];
+            }
+          }
+        }
+      }
+    }
+    tmem_wait_st();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tbase, a.tmem_cols);
+  }
+}
+
+static uint32_t pow2_cols(uint32_t c) {
+  uint32_t r = 32;
+  while (r < c) r <<= 1;
+  return r;
+}
+
+int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+                        const float* s0, int8_t* cfg, float* s_out, float* s_hist,
+                        cudaStream_t st) {
+  const nmfa_problem* p = pl->p;
+  SmallArgs a{};
+  a.j_img = reinterpret_cast<const uint4*>(p->d_j_small);
+  a.j_bytes = (uint32_t)p->np * p->np * 2;
+  a.invn = p->d_invn;
+  a.hn = p->d_hn;
+  a.inv_temp = pl->d_inv_temp;
+  a.n = (int)p->n;
+  a.np = p->np;
+  a.t_f = pl->t_f;
+  a.tmem_cols = pow2_cols(2u * p->np);
+  a.alpha = pl->alpha;
+  a.oma = pl->oma;
+  a.sigma = pl->sigma;
+  a.key_base = key_base;
+  a.R = pl->R;
+  a.noise = noise;
+  a.s0 = s0;
+  a.cfg = cfg;
+  a.s_out = s_out;
+  a.s_hist = s_hist;
+  const long long ctas = (pl->R + kRowsPerCta - 1) / kRowsPerCta;
+  // Spread columns over more warps when the grid cannot fill the GPU.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  a.cs = ctas >= 2 * sms ? 1 : (ctas >= sms ? 2 : 4);
+  if (a.cs > p->np / 16) a.cs = p->np / 16;
+  const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 + 16;
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(small_anneal_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  small_anneal_kernel<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
+  NMFA_LAUNCH_CHECK();
+  add_launches(1);
+  return NMFA_OK;
+}
+
+}  // namespace nmfa

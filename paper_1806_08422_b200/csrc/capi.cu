@@ -1,0 +1,505 @@
+// C-ABI layer: problem construction (problem.py:25-116 restated in C++),
+// plans, dispatch to the kernel paths, errors.  See include/nmfa_b200.h.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace nmfa {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+void add_launches(int64_t k) { g_launches += k; }
+
+static int arg_error(const std::string& msg) {
+  set_error(msg);
+  return NMFA_ERR_ARG;
+}
+
+template <class T>
+static int upload(T** dst, const T* src, size_t count) {
+  if (count == 0) count = 1;  // keep a valid pointer for empty arrays
+  NMFA_CUDA_TRY(cudaMalloc(dst, count * sizeof(T)));
+  if (src) NMFA_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  return NMFA_OK;
+}
+
+static bool exact_in_half(double v) {
+  __half h = __double2half(v);
+  return (double)__half2float(h) == v;
+}
+
+}  // namespace nmfa
+
+using namespace nmfa;
+
+extern "C" {
+
+const char* nmfa_last_error(void) { return g_err.c_str(); }
+const char* nmfa_version(void) { return "nmfa_b200 0.1.0 (sm_100a)"; }
+int64_t nmfa_last_launch_count(void) { return g_launches; }
+
+int nmfa_problem_destroy(nmfa_problem_t* p) {
+  if (!p) return NMFA_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  void* bufs[] = {p->d_invn, p->d_hn,    p->d_j_small, p->d_j_dense, p->d_csr_ptr, p->d_csr_idx,
+                  p->d_csr_w, p->d_e_i, p->d_e_j,     p->d_e_w,     p->d_h};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  cudaSetDevice(prev);
+  delete p;
+  return NMFA_OK;
+}
+
+int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const int64_t* ej_in,
+                        const double* w_in, const double* h_in, int32_t device,
+                        nmfa_problem_t** out) {
+  if (!out) return arg_error("out pointer is NULL");
+  *out = nullptr;
+  // ---- validation, problem.py:25-62 ----
+  if (n < 1) return arg_error("spin count must be positive, got " + std::to_string(n));
+  if (n > (int64_t)1 << 30) return arg_error("spin count too large");
+  if (n_edges < 0) return arg_error("couplers must be a sequence of (i, j, w) triples");
+  if (n_edges > 0 && (!ei_in || !ej_in || !w_in))
+    return arg_error("coupler arrays are NULL");
+  std::vector<double> h(n, 0.0);
+  if (h_in) {
+    for (int64_t i = 0; i < n; ++i) {
+      if (!std::isfinite(h_in[i])) return arg_error("h contains non-finite entries");
+      h[i] = h_in[i];
+    }
+  }
+  std::vector<int64_t> lo(n_edges), hi(n_edges);
+  std::vector<double> w(n_edges);
+  bool sorted = true;
+  for (int64_t k = 0; k < n_edges; ++k) {
+    int64_t a = ei_in[k], b = ej_in[k];
+    if (a < 0 || a >= n || b < 0 || b >= n)
+      return arg_error("coupler index out of range [0, " + std::to_string(n) + ")");
+    if (a == b) return arg_error("self-couplings are not allowed");
+    if (!std::isfinite(w_in[k])) return arg_error("coupler weights must be finite");
+    if (w_in[k] == 0.0) return arg_error("coupler weights must be nonzero");
+    lo[k] = std::min(a, b);
+    hi[k] = std::max(a, b);
+    w[k] = w_in[k];
+    if (k > 0 && (lo[k] < lo[k - 1] || (lo[k] == lo[k - 1] && hi[k] <= hi[k - 1])))
+      sorted = false;
+  }
+  if (!sorted) {  // canonical order: lexicographic (lo, hi), problem.py:63-66
+    std::vector<int64_t> perm(n_edges);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) {
+      return lo[x] != lo[y] ? lo[x] < lo[y] : hi[x] < hi[y];
+    });
+    std::vector<int64_t> lo2(n_edges), hi2(n_edges);
+    std::vector<double> w2(n_edges);
+    for (int64_t k = 0; k < n_edges; ++k) {
+      lo2[k] = lo[perm[k]];
+      hi2[k] = hi[perm[k]];
+      w2[k] = w[perm[k]];
+    }
+    lo.swap(lo2);
+    hi.swap(hi2);
+    w.swap(w2);
+  }
+  for (int64_t k = 1; k < n_edges; ++k)
+    if (lo[k] == lo[k - 1] && hi[k] == hi[k - 1])
+      return arg_error("duplicate coupler (" + std::to_string(lo[k]) + ", " +
+                       std::to_string(hi[k]) + ")");
+
+  auto* p = new nmfa_problem();
+  p->device = device;
+  p->n = n;
+  p->n_edges = n_edges;
+  int64_t pairs = n * (n - 1) / 2;
+  p->density = pairs == 0 ? 0.0 : (double)n_edges / (double)pairs;
+  p->is_dense = p->density > 0.5;
+  p->h = h;
+
+  // ---- symmetric CSR, rows sorted by column (problem.py:78-88) ----
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int64_t k = 0; k < n_edges; ++k) {
+    cnt[lo[k] + 1]++;
+    cnt[hi[k] + 1]++;
+  }
+  std::vector<int64_t> ptr(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + cnt[i + 1];
+  if (ptr[n] > INT32_MAX) {
+    delete p;
+    return arg_error("too many couplers for the int32 CSR");
+  }
+  std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+  std::vector<int32_t> cidx(ptr[n]);
+  std::vector<double> cw(ptr[n]);
+  // columns below the row first (edges with hi == row, increasing lo) ...
+  for (int64_t k = 0; k < n_edges; ++k) {
+    int64_t r = hi[k];
+    cidx[fill[r]] = (int32_t)lo[k];
+    cw[fill[r]++] = w[k];
+  }
+  // ... then columns above it (edges with lo == row, increasing hi)
+  for (int64_t k = 0; k < n_edges; ++k) {
+    int64_t r = lo[k];
+    cidx[fill[r]] = (int32_t)hi[k];
+    cw[fill[r]++] = w[k];
+  }
+  // ---- normalizers: np.bincount order (lo pass, then hi pass), problem.py:90-95 ----
+  std::vector<double> sq(n, 0.0);
+  for (int64_t k = 0; k < n_edges; ++k) sq[lo[k]] += w[k] * w[k];
+  for (int64_t k = 0; k < n_edges; ++k) sq[hi[k]] += w[k] * w[k];
+  p->norm_safe.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    double nr = std::sqrt(h[i] * h[i] + sq[i]);
+    p->norm_safe[i] = nr == 0.0 ? 1.0 : nr;
+  }
+
+  // ---- operand precision: J / 2^e exact in fp16? ----
+  double wmax = 0.0;
+  bool ints = true;
+  for (int64_t k = 0; k < n_edges; ++k) {
+    wmax = std::max(wmax, std::fabs(w[k]));
+    if (w[k] != std::floor(w[k])) ints = false;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (h[i] != std::floor(h[i])) ints = false;
+  p->int_weights = ints;
+  double scale = 1.0;
+  if (wmax > 0.0) {
+    bool exact1 = wmax <= 2048.0;
+    for (int64_t k = 0; k < n_edges && exact1; ++k) exact1 = exact_in_half(w[k]);
+    if (!exact1) scale = std::ldexp(1.0, (int)std::ceil(std::log2(wmax)));  // |J/scale| <= 1
+  }
+  p->j_scale = scale;
+  bool jex = true;
+  for (int64_t k = 0; k < n_edges && jex; ++k) jex = exact_in_half(w[k] / scale);
+  p->j_exact = jex;
+
+  int err = NMFA_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete p;
+    return arg_error("invalid CUDA device " + std::to_string(device));
+  }
+  do {
+    p->np = (int32_t)((n + 15) / 16 * 16);
+    std::vector<float> invn(p->np, 0.f), hn(p->np, 0.f);
+    for (int64_t i = 0; i < n; ++i) {
+      invn[i] = (float)(scale / p->norm_safe[i]);
+      hn[i] = (float)(h[i] / p->norm_safe[i]);
+    }
+    if ((err = upload(&p->d_invn, invn.data(), invn.size()))) break;
+    if ((err = upload(&p->d_hn, hn.data(), hn.size()))) break;
+
+    std::vector<int32_t> ptr32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) ptr32[i] = (int32_t)ptr[i];
+    std::vector<float> cw32(cw.size());
+    for (size_t k = 0; k < cw.size(); ++k) cw32[k] = (float)(cw[k] / scale);
+    if ((err = upload(&p->d_csr_ptr, ptr32.data(), ptr32.size()))) break;
+    if ((err = upload(&p->d_csr_idx, cidx.data(), cidx.size()))) break;
+    if ((err = upload(&p->d_csr_w, cw32.data(), cw32.size()))) break;
+
+    std::vector<int32_t> e_i(n_edges), e_j(n_edges);
+    for (int64_t k = 0; k < n_edges; ++k) {
+      e_i[k] = (int32_t)lo[k];
+      e_j[k] = (int32_t)hi[k];
+    }
+    if ((err = upload(&p->d_e_i, e_i.data(), e_i.size()))) break;
+    if ((err = upload(&p->d_e_j, e_j.data(), e_j.size()))) break;
+    if ((err = upload(&p->d_e_w, w.data(), w.size()))) break;
+    if ((err = upload(&p->d_h, h.data(), h.size()))) break;
+
+    if (n <= kSmallMaxN) {
+      // B operand image for the persistent kernel: B[row=i][k=j] = J_ij / scale
+      const uint32_t np = (uint32_t)p->np, lbo = np * 16u;
+      std::vector<__half> img((size_t)np * np, __float2half(0.f));
+      for (int64_t k = 0; k < n_edges; ++k) {
+        __half v = __double2half(w[k] / scale);
+        img[kmajor_off((uint32_t)lo[k], (uint32_t)hi[k], lbo) / 2] = v;
+        img[kmajor_off((uint32_t)hi[k], (uint32_t)lo[k], lbo) / 2] = v;
+      }
+      if ((err = upload(&p->d_j_small, img.data(), img.size()))) break;
+      p->path = NMFA_PATH_SMALL;
+    } else if (p->is_dense) {
+      std::vector<float> jd((size_t)n * n, 0.f);
+      for (int64_t k = 0; k < n_edges; ++k) {
+        float v = (float)(w[k] / scale);
+        jd[(size_t)lo[k] * n + hi[k]] = v;
+        jd[(size_t)hi[k] * n + lo[k]] = v;
+      }
+      if ((err = dense_problem_upload(p, jd))) break;
+      p->path = NMFA_PATH_DENSE;
+    } else {
+      p->path = NMFA_PATH_SPARSE;
+    }
+  } while (0);
+  cudaSetDevice(prev);
+  if (err) {
+    nmfa_problem_destroy(p);
+    return err;
+  }
+  *out = p;
+  return NMFA_OK;
+}
+
+int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
+  if (!p || !info) return arg_error("NULL argument");
+  info->n = p->n;
+  info->n_edges = p->n_edges;
+  info->density = p->density;
+  info->is_dense = p->is_dense;
+  info->path = p->path;
+  info->j_exact = p->j_exact;
+  info->int_weights = p->int_weights;
+  info->j_scale = p->j_scale;
+  return NMFA_OK;
+}
+
+int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
+  if (!p) return arg_error("NULL problem");
+  if (path == NMFA_PATH_SMALL && !p->d_j_small)
+    return arg_error("small path needs n <= 256");
+  if (path == NMFA_PATH_DENSE && !p->d_j_dense) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    std::vector<float> jd((size_t)p->n * p->n, 0.f);
+    std::vector<int32_t> e_i(p->n_edges), e_j(p->n_edges);
+    std::vector<double> w(p->n_edges);
+    int err = NMFA_OK;
+    if (p->n_edges) {
+      if (cudaMemcpy(e_i.data(), p->d_e_i, 4 * p->n_edges, cudaMemcpyDeviceToHost) ||
+          cudaMemcpy(e_j.data(), p->d_e_j, 4 * p->n_edges, cudaMemcpyDeviceToHost) ||
+          cudaMemcpy(w.data(), p->d_e_w, 8 * p->n_edges, cudaMemcpyDeviceToHost))
+        err = NMFA_ERR_CUDA;
+    }
+    if (!err) {
+      for (int64_t k = 0; k < p->n_edges; ++k) {
+        float v = (float)(w[k] / p->j_scale);
+        jd[(size_t)e_i[k] * p->n + e_j[k]] = v;
+        jd[(size_t)e_j[k] * p->n + e_i[k]] = v;
+      }
+      err = dense_problem_upload(p, jd);
+    }
+    cudaSetDevice(prev);
+    if (err) {
+      if (err == NMFA_ERR_CUDA && g_err.empty()) set_error("dense upload failed");
+      return err;
+    }
+  }
+  if (path < 0 || path > 2) return arg_error("unknown path");
+  p->path = path;
+  return NMFA_OK;
+}
+
+int nmfa_plan_destroy(nmfa_plan_t* pl) {
+  if (!pl) return NMFA_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->p->device);
+  void* bufs[] = {pl->d_inv_temp, pl->d_sa,    pl->d_sb,       pl->d_h16a,
+                  pl->d_h16b,     pl->d_bits,  pl->d_epart,    pl->d_hist_cfg};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  cudaSetDevice(prev);
+  delete pl;
+  return NMFA_OK;
+}
+
+int nmfa_plan_create(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
+                     double alpha, double sigma, nmfa_plan_t** out) {
+  if (!p || !out) return arg_error("NULL argument");
+  *out = nullptr;
+  if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
+  if (t_f < 1) return arg_error("t_f must be at least 1, got " + std::to_string(t_f));
+  if (!(alpha >= 0.0 && alpha <= 1.0))
+    return arg_error("alpha must be in [0, 1], got " + std::to_string(alpha));
+  if (!(sigma >= 0.0)) return arg_error("sigma must be nonnegative, got " + std::to_string(sigma));
+  if (!temps) return arg_error("temps is NULL");
+  std::vector<float> inv_t(t_f);
+  for (int32_t t = 0; t < t_f; ++t) {
+    if (!(temps[t] > 0.0) || !std::isfinite(temps[t]))
+      return arg_error("temperature must be positive, got " + std::to_string(temps[t]));
+    inv_t[t] = (float)(1.0 / temps[t]);
+  }
+  auto* pl = new nmfa_plan();
+  pl->p = p;
+  pl->R = R;
+  pl->t_f = t_f;
+  pl->alpha = (float)alpha;
+  pl->oma = (float)(1.0 - alpha);
+  pl->sigma = (float)sigma;
+  pl->h_inv_temp = inv_t;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  int err = NMFA_OK;
+  do {
+    if ((err = upload(&pl->d_inv_temp, inv_t.data(), inv_t.size()))) break;
+    if (p->path == NMFA_PATH_SPARSE) {
+      pl->Rp = (R + 31) / 32 * 32;
+      size_t bytes = (size_t)p->n * pl->Rp * sizeof(float);
+      if (cudaMalloc(&pl->d_sa, bytes) != cudaSuccess || cudaMalloc(&pl->d_sb, bytes) != cudaSuccess) {
+        set_error("out of device memory for sparse state");
+        err = NMFA_ERR_CUDA;
+        break;
+      }
+    } else if (p->path == NMFA_PATH_DENSE) {
+      if ((err = dense_plan_alloc(pl))) break;
+    }
+    int64_t chunks = energy_chunks_for(p, R);
+    pl->energy_chunks = chunks;
+    pl->bits_words = p->n * ((R + 31) / 32);
+    if (cudaMalloc(&pl->d_bits, pl->bits_words * 4) != cudaSuccess ||
+        cudaMalloc(&pl->d_epart, (size_t)(chunks + 1) * R * 8) != cudaSuccess) {
+      set_error("out of device memory for energy scratch");
+      err = NMFA_ERR_CUDA;
+      break;
+    }
+  } while (0);
+  cudaSetDevice(prev);
+  if (err) {
+    nmfa_plan_destroy(pl);
+    return err;
+  }
+  *out = pl;
+  return NMFA_OK;
+}
+
+int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise,
+                  const float* s0, int8_t* cfg, double* energy, float* s_out, float* s_hist,
+                  double* e_hist, void* stream) {
+  if (!pl) return arg_error("NULL plan");
+  if (!cfg) return arg_error("config output is NULL");
+  if (e_hist && !s_hist) return arg_error("e_hist requires s_hist");
+  g_launches = 0;
+  const nmfa_problem* p = pl->p;
+  cudaStream_t st = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  uint64_t key_base = seed + (uint64_t)r0;
+  int err = NMFA_OK;
+  switch (p->path) {
+    case NMFA_PATH_SMALL:
+      err = launch_small_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
+      break;
+    case NMFA_PATH_DENSE:
+      err = launch_dense_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
+      break;
+    default:
+      err = launch_sparse_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
+  }
+  if (!err && energy)
+    err = launch_energy(p, cfg, pl->R, energy, pl->d_bits, pl->d_epart, pl->energy_chunks, st);
+  if (!err && e_hist) {
+    // energies of sign(s_t) for every recorded step (_kernels_numba.py:57-60)
+    int64_t cnt = pl->R * (int64_t)pl->t_f;
+    int8_t* hc = nullptr;
+    uint32_t* hb = nullptr;
+    double* hp = nullptr;
+    int64_t ch = energy_chunks_for(p, cnt);
+    if (cudaMallocAsync(&hc, (size_t)cnt * p->n, st) != cudaSuccess ||
+        cudaMallocAsync(&hb, (size_t)p->n * ((cnt + 31) / 32) * 4, st) != cudaSuccess ||
+        cudaMallocAsync(&hp, (size_t)(ch + 1) * cnt * 8, st) != cudaSuccess) {
+      set_error("out of device memory for trajectory energies");
+      err = NMFA_ERR_CUDA;
+    } else {
+      err = launch_sign(s_hist, cnt * p->n, hc, st);
+      if (!err) err = launch_energy(p, hc, cnt, e_hist, hb, hp, ch, st);
+      cudaFreeAsync(hc, st);
+      cudaFreeAsync(hb, st);
+      cudaFreeAsync(hp, st);
+    }
+  }
+  cudaSetDevice(prev);
+  return err;
+}
+
+int nmfa_anneal(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
+                double alpha, double sigma, uint64_t seed, int64_t r0, const float* noise,
+                const float* s0, int8_t* cfg, double* energy, float* s_out, float* s_hist,
+                double* e_hist, void* stream) {
+  nmfa_plan_t* pl = nullptr;
+  int err = nmfa_plan_create(p, R, t_f, temps, alpha, sigma, &pl);
+  if (err) return err;
+  err = nmfa_plan_run(pl, seed, r0, noise, s0, cfg, energy, s_out, s_hist, e_hist, stream);
+  int64_t launches = g_launches;
+  if (!err && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
+    set_error(std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
+    err = NMFA_ERR_CUDA;
+  }
+  nmfa_plan_destroy(pl);
+  g_launches = launches;
+  return err;
+}
+
+int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
+                     double alpha, double sigma, uint64_t seed, int64_t r0, int8_t* cfg_host,
+                     double* energy_host) {
+  if (!p || !cfg_host) return arg_error("NULL argument");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  int8_t* d_cfg = nullptr;
+  double* d_e = nullptr;
+  int err = NMFA_OK;
+  if (cudaMalloc(&d_cfg, (size_t)R * p->n) != cudaSuccess ||
+      cudaMalloc(&d_e, (size_t)R * 8) != cudaSuccess) {
+    set_error("out of device memory");
+    err = NMFA_ERR_CUDA;
+  }
+  if (!err)
+    err = nmfa_anneal(p, R, t_f, temps, alpha, sigma, seed, r0, nullptr, nullptr, d_cfg,
+                      energy_host ? d_e : nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (!err && (cudaMemcpy(cfg_host, d_cfg, (size_t)R * p->n, cudaMemcpyDeviceToHost) ||
+               (energy_host &&
+                cudaMemcpy(energy_host, d_e, (size_t)R * 8, cudaMemcpyDeviceToHost)))) {
+    set_error("device to host copy failed");
+    err = NMFA_ERR_CUDA;
+  }
+  if (d_cfg) cudaFree(d_cfg);
+  if (d_e) cudaFree(d_e);
+  cudaSetDevice(prev);
+  return err;
+}
+
+int nmfa_energy(const nmfa_problem_t* p, const int8_t* cfg, int64_t n_cfg, double* energy,
+                void* stream) {
+  if (!p || !cfg || !energy) return arg_error("NULL argument");
+  if (n_cfg < 1) return arg_error("need at least one configuration");
+  cudaStream_t st = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  int64_t ch = energy_chunks_for(p, n_cfg);
+  uint32_t* bits = nullptr;
+  double* part = nullptr;
+  int err = NMFA_OK;
+  if (cudaMallocAsync(&bits, (size_t)p->n * ((n_cfg + 31) / 32) * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&part, (size_t)(ch + 1) * n_cfg * 8, st) != cudaSuccess) {
+    set_error("out of device memory");
+    err = NMFA_ERR_CUDA;
+  } else {
+    err = launch_energy(p, cfg, n_cfg, energy, bits, part, ch, st);
+  }
+  if (bits) cudaFreeAsync(bits, st);
+  if (part) cudaFreeAsync(part, st);
+  cudaSetDevice(prev);
+  return err;
+}
+
+int nmfa_best_of(const double* e, int64_t n, double* best_e, int64_t* best_i, void* stream) {
+  if (!e || !best_e || !best_i) return arg_error("NULL argument");
+  if (n < 1) return arg_error("best-of needs at least one energy");
+  return launch_best_of(e, n, best_e, best_i, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Internal (non-ABI) declarations shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/nmfa_b200.h"
+
+namespace nmfa {
+
+void set_error(const std::string& msg);
+void add_launches(int64_t k);
+
+#define NMFA_CUDA_TRY(expr)                                                          \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::nmfa::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " + \
+                        __FILE__ + ":" + std::to_string(__LINE__) + " (" #expr ")");  \
+      return NMFA_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+#define NMFA_LAUNCH_CHECK() NMFA_CUDA_TRY(cudaGetLastError())
+
+constexpr int kSmallMaxN = 256;  // persistent path keeps J (<=128 KB fp16) in SMEM
+
+}  // namespace nmfa
+
+// Device-resident immutable problem (mirrors IsingProblem, problem.py:16-138).
+struct nmfa_problem {
+  int32_t device = 0;
+  int64_t n = 0, n_edges = 0;
+  double density = 0.0;
+  bool is_dense = false;   // reference dispatch bit (problem.py:99)
+  int32_t path = NMFA_PATH_SPARSE;
+  bool j_exact = true;
+  bool int_weights = true;
+  double j_scale = 1.0;    // J_dev = J / j_scale (power of two); inv_norm carries j_scale
+  int32_t np = 0;          // n padded to a multiple of 16 (tensor-core paths)
+
+  std::vector<double> h, norm_safe;  // host copies (float64)
+
+  // per-spin epilogue constants, padded to np (zeros beyond n)
+  float* d_invn = nullptr;  // j_scale / norm_safe
+  float* d_hn = nullptr;    // h / norm_safe
+  // small path: B-operand image of J (K-major, no swizzle), np x np fp16
+  __half* d_j_small = nullptr;
+  // dense path: J tiles (see anneal_dense.cu for the layout)
+  __half* d_j_dense = nullptr;
+  size_t j_dense_bytes = 0;
+  // symmetric CSR, rows sorted by column (problem.py:78-88), J / j_scale in f32
+  int32_t* d_csr_ptr = nullptr;
+  int32_t* d_csr_idx = nullptr;
+  float* d_csr_w = nullptr;
+  // canonical upper edge list for the exact energy (problem.py:150-154)
+  int32_t* d_e_i = nullptr;
+  int32_t* d_e_j = nullptr;
+  double* d_e_w = nullptr;
+  double* d_h = nullptr;
+};
+
+struct nmfa_plan {
+  const nmfa_problem* p = nullptr;
+  int64_t R = 0;
+  int32_t t_f = 0;
+  float alpha = 0.f, oma = 0.f, sigma = 0.f;
+  float* d_inv_temp = nullptr;  // [t_f]
+  std::vector<float> h_inv_temp; // host copy (per-step launches read it)
+  // sparse / dense per-step state
+  int64_t Rp = 0;               // replica count padded for the state layout
+  float* d_sa = nullptr;        // master state ping
+  float* d_sb = nullptr;        // master state pong
+  __half* d_h16a = nullptr;     // dense path operand ping
+  __half* d_h16b = nullptr;     // dense path operand pong
+  uint32_t* d_bits = nullptr;   // energy: packed config bits
+  double* d_epart = nullptr;    // energy: partial sums
+  int64_t energy_chunks = 0;
+  int8_t* d_hist_cfg = nullptr; // trajectory energies: signs of s_hist
+  int64_t bits_words = 0;       // capacity of d_bits in uint32
+};
+
+namespace nmfa {
+// kernels (launchers return NMFA_OK or an error code)
+int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+                        const float* s0, int8_t* cfg, float* s_out, float* s_hist,
+                        cudaStream_t st);
+int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
+                         cudaStream_t st);
+int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+                        const float* s0, int8_t* cfg, float* s_out, float* s_hist,
+                        cudaStream_t st);
+int dense_plan_alloc(nmfa_plan* pl);
+int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jdense_rowmajor);
+int launch_energy(const nmfa_problem* p, const int8_t* cfg, int64_t n_cfg, double* energy,
+                  uint32_t* bits_scratch, double* part_scratch, int64_t chunks,
+                  cudaStream_t st);
+int64_t energy_chunks_for(const nmfa_problem* p, int64_t n_cfg);
+int launch_sign(const float* s, int64_t count, int8_t* cfg, cudaStream_t st);
+int launch_best_of(const double* e, int64_t n, double* best_e, int64_t* best_i,
+                   cudaStream_t st);
+}  // namespace nmfa

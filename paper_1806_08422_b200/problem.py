@@ -1,0 +1,280 @@
+"""Ising problem: the host-side mirror of the reference `nmfa.problem` API.
+
+`IsingProblem(n, couplers, h)` validates and canonicalises exactly like the
+reference (problem.py:25-116) and owns a device-resident handle per CUDA
+device (`nmfa_problem_create`, include/nmfa_b200.h).  The arithmetic helpers
+`energy` / `cut_value` evaluate on the GPU through the C-ABI (bit-exact for
+integer weights); `mean_field` / `normalizers` / `sign_round` are the same
+small host-side utilities the reference exposes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native
+
+DENSE_THRESHOLD = 0.5  # problem.py:13
+
+
+class IsingProblem:
+    """Immutable coupling structure: n spins, fields h, couplers (i, j, w)."""
+
+    def __init__(self, n, couplers=(), h=None):
+        n = int(n)
+        if n < 1:
+            raise ValueError(f"spin count must be positive, got {n}")
+        self.n = n
+        if h is None:
+            hv = np.zeros(n)
+        else:
+            hv = np.asarray(h, dtype=np.float64).copy()
+            if hv.shape != (n,):
+                raise ValueError(f"h must have length {n}, got shape {hv.shape}")
+            if not np.all(np.isfinite(hv)):
+                raise ValueError("h contains non-finite entries")
+        self.h = hv
+
+        arr = np.asarray(couplers, dtype=np.float64)
+        if arr.size == 0:
+            arr = np.empty((0, 3))
+        if arr.ndim != 2 or arr.shape[1] != 3:
+            raise ValueError("couplers must be a sequence of (i, j, w) triples")
+        ii, jj, ww = arr[:, 0], arr[:, 1], arr[:, 2].copy()
+        if not (np.all(ii == np.floor(ii)) and np.all(jj == np.floor(jj))):
+            raise ValueError("coupler indices must be integers")
+        self._init_edges(ii.astype(np.int64), jj.astype(np.int64), ww)
+
+    @classmethod
+    def from_arrays(cls, n, edges_i, edges_j, weights, h=None):
+        """Build from integer edge arrays without the (E, 3) float triple table."""
+        self = cls.__new__(cls)
+        n = int(n)
+        if n < 1:
+            raise ValueError(f"spin count must be positive, got {n}")
+        self.n = n
+        self.h = np.zeros(n) if h is None else np.asarray(h, dtype=np.float64).copy()
+        if self.h.shape != (n,):
+            raise ValueError(f"h must have length {n}, got shape {self.h.shape}")
+        if not np.all(np.isfinite(self.h)):
+            raise ValueError("h contains non-finite entries")
+        self._init_edges(np.asarray(edges_i, dtype=np.int64), np.asarray(edges_j, dtype=np.int64),
+                         np.asarray(weights, dtype=np.float64).copy())
+        return self
+
+    def _init_edges(self, ii, jj, ww):
+        n = self.n
+        if np.any((ii < 0) | (ii >= n) | (jj < 0) | (jj >= n)):
+            raise ValueError(f"coupler index out of range [0, {n})")
+        if np.any(ii == jj):
+            raise ValueError("self-couplings are not allowed")
+        if not np.all(np.isfinite(ww)):
+            raise ValueError("coupler weights must be finite")
+        if np.any(ww == 0.0):
+            raise ValueError("coupler weights must be nonzero")
+        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+        key = lo * n + hi
+        if key.size > 1 and not np.all(key[1:] > key[:-1]):
+            order = np.argsort(key, kind="stable")       # canonical (lo, hi) order
+            lo, hi, ww, key = lo[order], hi[order], ww[order], key[order]
+            dup = key[1:] == key[:-1]
+            if np.any(dup):
+                k = int(np.flatnonzero(dup)[0])
+                raise ValueError(f"duplicate coupler ({lo[k]}, {hi[k]})")
+        self.edges_i, self.edges_j, self.edge_weights = lo, hi, ww
+        pairs = n * (n - 1) // 2
+        self.density = 0.0 if pairs == 0 else lo.size / pairs
+        self.is_dense = self.density > DENSE_THRESHOLD
+        for a in (self.h, self.edges_i, self.edges_j, self.edge_weights):
+            a.flags.writeable = False
+        self._handles = {}
+        self._hlock = threading.Lock()
+        self._csr = None
+
+    # ---- reference-compatible views (problem.py:78-138), built on demand ----
+    def _build_csr(self):
+        if self._csr is None:
+            lo, hi, ww = self.edges_i, self.edges_j, self.edge_weights
+            rows = np.concatenate([lo, hi])
+            cols = np.concatenate([hi, lo])
+            vals = np.concatenate([ww, ww])
+            perm = np.lexsort((cols, rows))
+            indptr = np.zeros(self.n + 1, dtype=np.int64)
+            np.cumsum(np.bincount(rows, minlength=self.n), out=indptr[1:])
+            norm = np.sqrt(self.h ** 2 + np.bincount(rows, weights=vals ** 2, minlength=self.n))
+            self._csr = (indptr, cols[perm], vals[perm], norm)
+        return self._csr
+
+    @property
+    def csr_indptr(self):
+        return self._build_csr()[0]
+
+    @property
+    def csr_indices(self):
+        return self._build_csr()[1]
+
+    @property
+    def csr_weights(self):
+        return self._build_csr()[2]
+
+    @property
+    def normalizers_safe(self):
+        norm = self._build_csr()[3]
+        return np.where(norm == 0.0, 1.0, norm)
+
+    @property
+    def dense_weights(self):
+        if not self.is_dense:
+            return None
+        J = np.zeros((self.n, self.n))
+        J[self.edges_i, self.edges_j] = self.edge_weights
+        J[self.edges_j, self.edges_i] = self.edge_weights
+        return J
+
+    @property
+    def num_edges(self):
+        return int(self.edges_i.size)
+
+    @property
+    def w_total(self):
+        return float(self.edge_weights.sum())
+
+    def neighbors(self, i):
+        indptr, idx, w, _ = self._build_csr()
+        a, b = indptr[i], indptr[i + 1]
+        return idx[a:b], w[a:b]
+
+    def matvec(self, s):
+        indptr, idx, w, _ = self._build_csr()
+        s = np.asarray(s, dtype=np.float64)
+        out = np.zeros(self.n)
+        np.add.at(out, np.repeat(np.arange(self.n), np.diff(indptr)), w * s[idx])
+        return out
+
+    def __repr__(self):
+        return f"IsingProblem(n={self.n}, edges={self.num_edges})"
+
+    # ---- device handle ----
+    def device_handle(self, device=0):
+        """The immutable device-resident problem on `device` (created once)."""
+        device = int(device)
+        with self._hlock:
+            h = self._handles.get(device)
+            if h is None:
+                lib = _native.load()
+                out = ctypes.c_void_p()
+                ei = np.ascontiguousarray(self.edges_i, dtype=np.int64)
+                ej = np.ascontiguousarray(self.edges_j, dtype=np.int64)
+                w = np.ascontiguousarray(self.edge_weights, dtype=np.float64)
+                hv = np.ascontiguousarray(self.h, dtype=np.float64)
+                _native.check(lib.nmfa_problem_create(
+                    self.n, int(ei.size), _native.ptr(ei), _native.ptr(ej), _native.ptr(w),
+                    _native.ptr(hv), device, ctypes.byref(out)))
+                h = _DeviceProblem(out, device)
+                self._handles[device] = h
+            return h
+
+    def device_info(self, device=0):
+        return self.device_handle(device).info()
+
+
+class _DeviceProblem:
+    def __init__(self, handle, device):
+        self.handle = handle
+        self.device = device
+
+    def info(self):
+        info = _native.ProblemInfo()
+        _native.check(_native.load().nmfa_problem_get_info(self.handle, ctypes.byref(info)))
+        return {"n": info.n, "n_edges": info.n_edges, "density": info.density,
+                "is_dense": bool(info.is_dense), "path": _native.PATH_NAMES[info.path],
+                "j_exact": bool(info.j_exact), "int_weights": bool(info.int_weights),
+                "j_scale": info.j_scale}
+
+    def set_path(self, path):
+        code = {v: k for k, v in _native.PATH_NAMES.items()}[path]
+        _native.check(_native.load().nmfa_problem_set_path(self.handle, code))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _native.load().nmfa_problem_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def as_problem(obj):
+    """Accept our IsingProblem or any object with the reference's fields."""
+    if isinstance(obj, IsingProblem):
+        return obj
+    cached = getattr(obj, "_nmfa_b200_problem", None)
+    if cached is not None:
+        return cached
+    p = IsingProblem.from_arrays(obj.n, obj.edges_i, obj.edges_j, obj.edge_weights, obj.h)
+    try:
+        object.__setattr__(obj, "_nmfa_b200_problem", p)
+    except Exception:
+        pass
+    return p
+
+
+def _check_length(problem, v, what):
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape[-1:] != (problem.n,):
+        raise ValueError(f"{what} length {v.shape} does not match problem size {problem.n}")
+    return v
+
+
+def energies(problem, configs, device=0):
+    """GPU energies of a (R, n) batch of +-1 configurations (float64)."""
+    import torch
+
+    problem = as_problem(problem)
+    c = _check_length(problem, configs, "configuration")
+    c2 = np.atleast_2d(c)
+    cfg = torch.from_numpy(np.where(c2 < 0.0, -1, 1).astype(np.int8)).to(f"cuda:{device}")
+    out = torch.empty(cfg.shape[0], dtype=torch.float64, device=cfg.device)
+    stream = torch.cuda.current_stream(cfg.device).cuda_stream
+    _native.check(_native.load().nmfa_energy(problem.device_handle(device).handle,
+                                             _native.ptr(cfg), cfg.shape[0], _native.ptr(out),
+                                             ctypes.c_void_p(stream)))
+    return out.cpu().numpy()
+
+
+def energy(problem, config, device=0):
+    """Ising energy sum_(i<j) w s_i s_j + sum_i h_i s_i of a +-1 config (problem.py:150)."""
+    c = np.asarray(config, dtype=np.float64)
+    problem = as_problem(problem)
+    if c.shape != (problem.n,):
+        raise ValueError(
+            f"configuration length {c.shape} does not match problem size {problem.n}")
+    return float(energies(problem, c[None, :], device)[0])
+
+
+def cut_value(problem, config, device=0):
+    """Total weight of cut edges; requires h = 0 (problem.py:157-163)."""
+    problem = as_problem(problem)
+    if np.any(problem.h != 0.0):
+        raise ValueError("cut value is only defined for problems with zero fields")
+    return (problem.w_total - energy(problem, config, device)) * 0.5
+
+
+def mean_field(problem, s):
+    """Raw mean field phi_i = h_i + sum_j J_ij s_j (problem.py:166-169)."""
+    problem = as_problem(problem)
+    v = _check_length(problem, s, "spin vector")
+    return problem.h + problem.matvec(v)
+
+
+def normalizers(problem):
+    """sqrt(h_i^2 + sum_j J_ij^2); zero for isolated field-free spins (problem.py:172)."""
+    return as_problem(problem)._build_csr()[3].copy()
+
+
+def sign_round(s):
+    """Round analog spins to +-1; exact zeros map to +1 (problem.py:181-183)."""
+    return np.where(np.asarray(s, dtype=np.float64) < 0.0, -1.0, 1.0)

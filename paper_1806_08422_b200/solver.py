@@ -1,0 +1,365 @@
+"""NMFA sampling entry points -- drop-in mirror of the reference `nmfa.solver`.
+
+Same names, arguments, defaults and error behaviour as the reference
+(solver.py:41-280): `Schedule`, `NmfaParams`, `RunResult`, `Trajectory`,
+`noise_stream`, `run_with_noise`, `nmfa_step`, `nmfa_run`, `nmfa_batch`.
+Every anneal runs on the GPU through the C-ABI (`_native`); there is no CPU
+path.  Differences, all documented in DESIGN.md:
+
+* Seeded runs draw their noise in-kernel from a counter-based Philox4x32-10
+  stream keyed by (seed + replica) instead of numpy's sequential Philox4x64 +
+  ziggurat, so a given seed reproduces the reference statistically, not
+  bitwise.  Bitwise-comparable noise goes through `run_with_noise` (the
+  reference's own injected-noise seam) or `nmfa_step` (which draws from the
+  caller's numpy generator exactly like the reference).
+* `nmfa_batch` runs all replicas in one device batch; `threads` is accepted
+  for signature compatibility and ignored (results never depended on it).
+* `run_with_noise` additionally accepts a batch of noise (R, t_f, n) and then
+  returns (R, n) spins and a list of trajectories.
+* `sample()` is the batched API underneath: device tensors in and out.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native
+from .problem import as_problem, energy  # noqa: F401  (re-exported like the reference)
+
+MASK64 = (1 << 64) - 1
+RUN_STREAM_TAG = 2                     # solver.py:33 (numpy noise_stream key space)
+DEFAULT_ALPHA = 0.15
+DEFAULT_SIGMA = 0.15
+DEFAULT_TF = 1000
+
+
+class Schedule:
+    """Piecewise exponential temperature curve over the anneal fraction (solver.py:41-127)."""
+
+    def __init__(self, breakpoints):
+        pts = [(float(f), float(T)) for f, T in breakpoints]
+        if len(pts) < 2:
+            raise ValueError("schedule needs at least two breakpoints")
+        fs = np.array([f for f, _ in pts])
+        Ts = np.array([T for _, T in pts])
+        if fs[0] != 0.0 or fs[-1] != 1.0:
+            raise ValueError("schedule must start at f=0 and end at f=1")
+        if np.any(np.diff(fs) <= 0.0):
+            raise ValueError("schedule fractions must be strictly increasing")
+        if np.any(Ts <= 0.0) or not np.all(np.isfinite(Ts)):
+            raise ValueError("schedule temperatures must be positive and finite")
+        self._fs, self._Ts = fs, Ts
+        self._fs.flags.writeable = False
+        self._Ts.flags.writeable = False
+
+    @property
+    def breakpoints(self):
+        return tuple(zip(self._fs.tolist(), self._Ts.tolist()))
+
+    def temperatures(self, t_f):
+        """Temperatures for iterations t = 1..t_f (host float64, uploaded once)."""
+        t_f = int(t_f)
+        if t_f < 1:
+            raise ValueError("t_f must be at least 1")
+        f = np.zeros(1) if t_f == 1 else np.arange(t_f) / (t_f - 1)
+        fs, Ts = self._fs, self._Ts
+        k = np.clip(np.searchsorted(fs, f, side="right") - 1, 0, len(fs) - 2)
+        frac = (f - fs[k]) / (fs[k + 1] - fs[k])
+        out = Ts[k] * (Ts[k + 1] / Ts[k]) ** frac
+        out[f >= fs[-1]] = Ts[-1]
+        return out
+
+    def temperature(self, t, t_f):
+        t, t_f = int(t), int(t_f)
+        if t_f < 1:
+            raise ValueError("t_f must be at least 1")
+        if not 1 <= t <= t_f:
+            raise ValueError(f"iteration {t} outside [1, {t_f}]")
+        f = 0.0 if t_f == 1 else (t - 1) / (t_f - 1)
+        fs, Ts = self._fs, self._Ts
+        if f >= fs[-1]:
+            return float(Ts[-1])
+        k = min(max(int(np.searchsorted(fs, f, side="right")) - 1, 0), len(fs) - 2)
+        frac = (f - fs[k]) / (fs[k + 1] - fs[k])
+        return float(Ts[k] * (Ts[k + 1] / Ts[k]) ** frac)
+
+    @classmethod
+    def parse(cls, text):
+        """Parse "f:T,f:T,..." (e.g. "0:2,0.25:0.8,0.75:0.2,1:0.02")."""
+        pts = []
+        for part in text.split(","):
+            part = part.strip()
+            if not part:
+                continue
+            bits = part.split(":")
+            if len(bits) != 2:
+                raise ValueError(f"bad schedule point {part!r}, expected f:T")
+            try:
+                pts.append((float(bits[0]), float(bits[1])))
+            except ValueError:
+                raise ValueError(f"bad schedule point {part!r}, expected f:T") from None
+        return cls(pts)
+
+    def format(self):
+        return ",".join(f"{f:g}:{T:g}" for f, T in self.breakpoints)
+
+    def __repr__(self):
+        return f"Schedule({self.format()!r})"
+
+    def __eq__(self, other):
+        return isinstance(other, Schedule) and self.breakpoints == other.breakpoints
+
+    def __hash__(self):
+        return hash(self.breakpoints)
+
+
+DEFAULT_SCHEDULE = Schedule([(0.0, 2.0), (0.25, 0.8), (0.75, 0.2), (1.0, 0.02)])
+
+
+def schedule_eval(schedule, t, t_f):
+    """Temperature at iteration t of t_f (t is 1-based)."""
+    return schedule.temperature(t, t_f)
+
+
+@dataclass(frozen=True)
+class NmfaParams:
+    """Solver parameters: feedback alpha, noise sigma, length t_f, schedule, seed."""
+
+    alpha: float = DEFAULT_ALPHA
+    sigma: float = DEFAULT_SIGMA
+    t_f: int = DEFAULT_TF
+    schedule: Schedule = DEFAULT_SCHEDULE
+    seed: int = 0
+
+    def __post_init__(self):
+        if not 0.0 <= self.alpha <= 1.0:
+            raise ValueError(f"alpha must be in [0, 1], got {self.alpha}")
+        if self.sigma < 0.0:
+            raise ValueError(f"sigma must be nonnegative, got {self.sigma}")
+        if int(self.t_f) < 1:
+            raise ValueError(f"t_f must be at least 1, got {self.t_f}")
+        object.__setattr__(self, "t_f", int(self.t_f))
+        if not 0 <= int(self.seed) <= MASK64:
+            raise ValueError("seed must fit in 64 unsigned bits")
+        object.__setattr__(self, "seed", int(self.seed))
+
+
+@dataclass(frozen=True)
+class Trajectory:
+    """Per-iteration record: analog spins and the energy of their rounding."""
+
+    spins: np.ndarray      # (t_f, n)
+    energies: np.ndarray   # (t_f,)
+
+
+@dataclass(frozen=True)
+class RunResult:
+    final_config: np.ndarray
+    final_energy: float
+    seed: int
+    wall_clock: float      # seconds per run: batch wall / n_runs (SPEC tau convention)
+    trajectory: Trajectory | None = None
+
+
+def noise_stream(seed):
+    """numpy Philox generator with the reference's stream identity (solver.py:182-185).
+
+    Only used to draw host noise for the injected-noise seam (`nmfa_step`);
+    seeded anneals draw in-kernel noise instead.
+    """
+    key = (RUN_STREAM_TAG << 64) | (int(seed) & MASK64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+# ---------------------------------------------------------------------------
+# batched device API
+# ---------------------------------------------------------------------------
+class Plan:
+    """Device state for n_runs replicas x t_f steps of one problem (nmfa_plan_*)."""
+
+    def __init__(self, problem, n_runs, temps, alpha, sigma, device=0):
+        self.problem = as_problem(problem)
+        self.dev = self.problem.device_handle(device)
+        self.device = int(device)
+        self.n_runs = int(n_runs)
+        self.temps = np.ascontiguousarray(temps, dtype=np.float64)
+        self.t_f = int(self.temps.size)
+        self.alpha, self.sigma = float(alpha), float(sigma)
+        out = ctypes.c_void_p()
+        _native.check(_native.load().nmfa_plan_create(
+            self.dev.handle, self.n_runs, self.t_f, _native.ptr(self.temps), self.alpha,
+            self.sigma, ctypes.byref(out)))
+        self.handle = out
+
+    def run(self, seed, r0=0, noise=None, s0=None, config=None, energy=None, s_final=None,
+            s_hist=None, e_hist=None, stream=None):
+        """Enqueue one batch on `stream` (a torch.cuda.Stream or None = current)."""
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        _native.check(_native.load().nmfa_plan_run(
+            self.handle, int(seed) & MASK64, int(r0), _native.ptr(noise), _native.ptr(s0),
+            _native.ptr(config), _native.ptr(energy), _native.ptr(s_final),
+            _native.ptr(s_hist), _native.ptr(e_hist), ctypes.c_void_p(stream.cuda_stream)))
+        return _native.load().nmfa_last_launch_count()
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _native.load().nmfa_plan_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+@dataclass
+class SampleSet:
+    """Batched result of `sample`: device tensors plus timing."""
+
+    configs: "object"          # torch.int8 (R, n) on device, values +-1
+    energies: "object"         # torch.float64 (R,) on device
+    seed: int
+    r0: int
+    wall_clock: float          # seconds for the whole batch
+    s_final: "object" = None   # torch.float32 (R, n) or None
+    s_hist: "object" = None    # torch.float32 (R, t_f, n) or None
+    e_hist: "object" = None    # torch.float64 (R, t_f) or None
+
+    def best(self):
+        """(best energy, global replica index) -- best-of-reads on device."""
+        import torch
+
+        be = torch.empty(1, dtype=torch.float64, device=self.energies.device)
+        bi = torch.empty(1, dtype=torch.int64, device=self.energies.device)
+        stream = torch.cuda.current_stream(self.energies.device)
+        _native.check(_native.load().nmfa_best_of(
+            _native.ptr(self.energies), self.energies.numel(), _native.ptr(be), _native.ptr(bi),
+            ctypes.c_void_p(stream.cuda_stream)))
+        return float(be.item()), int(bi.item()) + self.r0
+
+
+def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=None,
+           temps=None, return_s=False, record_trajectory=False):
+    """Run n_runs replicas (global indices r0..r0+n_runs-1) in one device batch.
+
+    noise: optional (n_runs, t_f, n) pre-scaled additive noise (device tensor
+    or array); when given, params.sigma is unused (run_with_noise seam).
+    """
+    import torch
+
+    params = NmfaParams() if params is None else params
+    problem = as_problem(problem)
+    n = problem.n
+    n_runs = int(n_runs)
+    if n_runs < 1:
+        raise ValueError(f"n_runs must be at least 1, got {n_runs}")
+    temps = params.schedule.temperatures(params.t_f) if temps is None else np.asarray(
+        temps, dtype=np.float64)
+    t_f = int(temps.size)
+    dev = torch.device(f"cuda:{device}")
+    if noise is not None:
+        noise = torch.as_tensor(noise, dtype=torch.float32, device=dev).contiguous()
+        if tuple(noise.shape) != (n_runs, t_f, n):
+            raise ValueError(f"noise shape {tuple(noise.shape)} does not match "
+                             f"({n_runs}, {t_f}, {n})")
+    if s0 is not None:
+        s0 = torch.as_tensor(s0, dtype=torch.float32, device=dev).contiguous()
+        if tuple(s0.shape) != (n_runs, n):
+            raise ValueError(f"s0 length does not match problem size {n}")
+    plan = Plan(problem, n_runs, temps, params.alpha, params.sigma, device)
+    cfg = torch.empty((n_runs, n), dtype=torch.int8, device=dev)
+    en = torch.empty(n_runs, dtype=torch.float64, device=dev)
+    s_final = torch.empty((n_runs, n), dtype=torch.float32, device=dev) if return_s else None
+    s_hist = e_hist = None
+    if record_trajectory:
+        s_hist = torch.empty((n_runs, t_f, n), dtype=torch.float32, device=dev)
+        e_hist = torch.empty((n_runs, t_f), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    plan.run(params.seed, r0, noise, s0, cfg, en, s_final, s_hist, e_hist)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    return SampleSet(cfg, en, int(params.seed), int(r0), wall, s_final, s_hist, e_hist)
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible entry points
+# ---------------------------------------------------------------------------
+def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=False, device=0):
+    """Anneal with caller-supplied, pre-scaled noise (solver.py:188-218).
+
+    noise (t_f, n) -> returns (s (n,), Trajectory | None), like the reference.
+    noise (R, t_f, n) -> returns (S (R, n), list[Trajectory] | None).
+    """
+    problem = as_problem(problem)
+    temps = np.asarray(temps, dtype=np.float64)
+    noise = np.asarray(noise, dtype=np.float64)
+    batched = noise.ndim == 3
+    nz = noise if batched else noise[None]
+    if nz.shape[1:] != (temps.shape[0], problem.n):
+        shape = noise.shape
+        raise ValueError(f"noise shape {shape} does not match ({temps.shape[0]}, {problem.n})")
+    R = nz.shape[0]
+    if s0 is not None:
+        s0 = np.array(s0, dtype=np.float64)
+        want = (R, problem.n) if batched else (problem.n,)
+        if s0.shape != want:
+            raise ValueError(f"s0 length does not match problem size {problem.n}")
+        s0 = s0.reshape(R, problem.n)
+    params = NmfaParams(alpha=float(alpha), sigma=1.0, t_f=temps.shape[0])
+    res = sample(problem, params, R, device=device, noise=nz.astype(np.float32), s0=s0,
+                 temps=temps, return_s=True, record_trajectory=record_trajectory)
+    S = res.s_final.double().cpu().numpy()
+    trajs = None
+    if record_trajectory:
+        sh = res.s_hist.double().cpu().numpy()
+        eh = res.e_hist.cpu().numpy()
+        trajs = [Trajectory(spins=sh[r], energies=eh[r]) for r in range(R)]
+    if batched:
+        return S, trajs
+    return S[0], (trajs[0] if trajs else None)
+
+
+def nmfa_step(problem, s, T, params, rng):
+    """One synchronous update at temperature T; noise from `rng` (solver.py:221-233)."""
+    if T <= 0.0:
+        raise ValueError(f"temperature must be positive, got {T}")
+    problem = as_problem(problem)
+    noise = rng.standard_normal(problem.n) * params.sigma
+    s_new, _ = run_with_noise(problem, np.array([float(T)]), noise[None, :], params.alpha, s0=s)
+    return s_new
+
+
+def _results(problem, res, params, record_trajectory):
+    cfg = res.configs.cpu().numpy().astype(np.float64)
+    en = res.energies.cpu().numpy()
+    R = cfg.shape[0]
+    per = res.wall_clock / R
+    trajs = [None] * R
+    if record_trajectory:
+        sh = res.s_hist.double().cpu().numpy()
+        eh = res.e_hist.cpu().numpy()
+        trajs = [Trajectory(spins=sh[r], energies=eh[r]) for r in range(R)]
+    return [RunResult(final_config=cfg[r], final_energy=float(en[r]),
+                      seed=(params.seed + res.r0 + r) & MASK64, wall_clock=per,
+                      trajectory=trajs[r]) for r in range(R)]
+
+
+def nmfa_run(problem, params, record_trajectory=False, device=0):
+    """Full anneal from all-zero spins; deterministic given (problem, seed)."""
+    res = sample(problem, params, 1, device=device, record_trajectory=record_trajectory)
+    return _results(problem, res, params, record_trajectory)[0]
+
+
+def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, device=0):
+    """n_runs independent anneals; run k uses seed params.seed + k (solver.py:262-280)."""
+    n_runs = int(n_runs)
+    if n_runs < 1:
+        raise ValueError(f"n_runs must be at least 1, got {n_runs}")
+    res = sample(problem, params, n_runs, device=device, record_trajectory=record_trajectory)
+    return _results(problem, res, params, record_trajectory)

@@ -1,0 +1,59 @@
+"""The C-ABI library loads and exports every symbol include/nmfa_b200.h declares."""
+
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1806_08422_b200 import _native
+from paper_1806_08422_b200 import build as nbuild
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "nmfa_b200.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(nmfa_\w+)\s*\(", txt, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    nbuild.build()
+    return _native.load()
+
+
+def test_header_declares_expected_surface():
+    names = declared()
+    assert "nmfa_plan_run" in names and "nmfa_best_of" in names and len(names) >= 12
+    assert set(names) == set(_native.SIGNATURES), "binding table out of sync with header"
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (nmfa_\w+)", out))
+    missing = [n for n in declared() if n not in exported]
+    assert not missing, missing
+
+
+def test_version_and_error_without_gpu(lib):
+    assert lib.nmfa_version().startswith(b"nmfa_b200")
+    with pytest.raises(ValueError):
+        _native.check(lib.nmfa_best_of(None, 0, None, None, None))
+    assert b"NULL" in lib.nmfa_last_error()
+
+
+def test_problem_create_rejects_bad_arguments(lib):
+    import ctypes
+    import numpy as np
+    out = ctypes.c_void_p()
+    ei = np.array([0], dtype=np.int64)
+    ej = np.array([0], dtype=np.int64)
+    w = np.array([1.0])
+    with pytest.raises(ValueError, match="self-couplings"):
+        _native.check(lib.nmfa_problem_create(2, 1, _native.ptr(ei), _native.ptr(ej),
+                                              _native.ptr(w), None, 0, ctypes.byref(out)))
+    with pytest.raises(ValueError, match="positive"):
+        _native.check(lib.nmfa_problem_create(0, 0, None, None, None, None, 0, ctypes.byref(out)))

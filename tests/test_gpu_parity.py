@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path through the C ABI against the reference-pinned oracle.
+
+Tolerances: the device state is fp32 with an fp16
+tensor-core operand, the reference is float64, so trajectories under the
+same injected noise agree to |dS| <= 2e-2 with identical final signs wherever
+the reference spin is not within 2e-2 of zero; energies are bit-exact for
+integer weights; seeded statistics agree within binomial confidence bounds.
+"""
+
+import numpy as np
+import pytest
+
+import nmfa_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1806_08422_b200 as nb  # noqa: E402
+from paper_1806_08422_b200 import _native  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1806_08422_b200 import build
+    build.build()
+    _native.load()
+
+
+def eprob(G, name):
+    E = G["energies"]
+    return nb.IsingProblem.from_arrays(int(E[name + "_n"]), E[name + "_ei"], E[name + "_ej"],
+                                       E[name + "_w"], E[name + "_h"])
+
+
+def oprob(G, name):
+    E = G["energies"]
+    return O.problem_from_edges(int(E[name + "_n"]), E[name + "_ei"], E[name + "_ej"],
+                                E[name + "_w"], E[name + "_h"])
+
+
+TRAJ = ["moebius16", "cubic40_s1", "sk30_s2", "dense60_p03_s3", "int40_h", "real24_h", "sk100_s0"]
+
+
+def assert_traj_close(s_gpu, s_ref, tol=2e-2):
+    s_gpu, s_ref = np.asarray(s_gpu), np.asarray(s_ref)
+    assert np.max(np.abs(s_gpu - s_ref)) <= tol, np.max(np.abs(s_gpu - s_ref))
+    firm = np.abs(s_ref) > tol
+    assert np.array_equal(np.sign(s_gpu[firm]), np.sign(s_ref[firm]))
+
+
+@pytest.mark.parametrize("name", TRAJ)
+@pytest.mark.parametrize("path", ["small", "sparse"])
+def test_injected_noise_trajectory_matches_reference(G, name, path):
+    T = G["trajectories"]
+    p = eprob(G, name)
+    p.device_handle().set_path(path)
+    t_f, seed = int(T[name + "_tf"]), int(T[name + "_seed"])
+    noise = O.run_noise(seed, t_f, p.n, 0.15)
+    s, tr = nb.run_with_noise(p, O.temperatures(t_f), noise, 0.15, record_trajectory=True)
+    assert_traj_close(s, T[name + "_s"])
+    assert_traj_close(tr.spins[-10:], T[name + "_s_hist_last10"])
+    # trajectory energies are exact energies of the GPU's own rounded spins
+    op = oprob(G, name)
+    want = O.energies(op, O.sign_round(tr.spins))
+    if op.edge_weights.dtype.kind == "f" and np.all(op.edge_weights == np.round(op.edge_weights)) \
+            and np.all(op.h == np.round(op.h)):
+        assert np.array_equal(tr.energies, want)
+    else:
+        assert np.allclose(tr.energies, want, rtol=1e-12, atol=1e-12)
+    # ... and agree with the reference's trajectory energies at almost every step
+    agree = np.mean(tr.energies == T[name + "_e_hist"]) if name != "real24_h" else \
+        np.mean(np.isclose(tr.energies, T[name + "_e_hist"], rtol=1e-9))
+    assert agree >= 0.9, agree
+
+
+@pytest.mark.parametrize("name", ["moebius16", "cubic40_s1", "sk30_s2", "sk100_s0"])
+@pytest.mark.parametrize("path", ["small", "sparse"])
+def test_noise_negation_is_exact(G, name, path):
+    p = eprob(G, name)
+    p.device_handle().set_path(path)
+    noise = O.run_noise(3, 80, p.n, 0.15)
+    temps = O.temperatures(80)
+    s_pos, tp = nb.run_with_noise(p, temps, noise, 0.15, record_trajectory=True)
+    s_neg, tn = nb.run_with_noise(p, temps, -noise, 0.15, record_trajectory=True)
+    assert np.array_equal(s_neg, -s_pos)
+    assert np.array_equal(tn.spins, -tp.spins)
+
+
+def test_batched_noise_equals_single_runs(G):
+    p = eprob(G, "sk30_s2")
+    temps = O.temperatures(50)
+    noise = np.stack([O.run_noise(s, 50, p.n, 0.15) for s in range(5)])
+    S, _ = nb.run_with_noise(p, temps, noise, 0.15)
+    for r in range(5):
+        s1, _ = nb.run_with_noise(p, temps, noise[r], 0.15)
+        assert np.array_equal(S[r], s1)
+
+
+def test_identity_step_and_validation():
+    p = nb.IsingProblem(2, [(0, 1, 1.0)])
+    s0 = np.array([0.25, -0.5])
+    s, _ = nb.run_with_noise(p, np.full(10, 0.5), np.zeros((10, 2)), 0.0, s0=s0)
+    assert np.array_equal(s, s0)
+    with pytest.raises(ValueError, match="noise shape"):
+        nb.run_with_noise(p, np.array([1.0]), np.zeros((2, 2)), 0.15)
+    with pytest.raises(ValueError, match="s0 length"):
+        nb.run_with_noise(p, np.array([1.0]), np.zeros((1, 2)), 0.15, s0=np.zeros(3))
+    with pytest.raises(ValueError):
+        nb.nmfa_step(p, np.zeros(2), 0.0, nb.NmfaParams(), nb.noise_stream(0))
+    with pytest.raises(ValueError):
+        nb.nmfa_batch(p, nb.NmfaParams(), 0)
+
+
+def test_tanh_kat(G):
+    p = nb.IsingProblem(2, [(0, 1, 1.0)])
+    out = nb.nmfa_step(p, np.array([0.9, 0.9]), 0.5, nb.NmfaParams(alpha=1.0, sigma=0.0, t_f=1),
+                       nb.noise_stream(0))
+    assert out == pytest.approx([-0.94681, -0.94681], abs=1e-5)
+    assert np.allclose(out, G["trajectories"]["kat_tanh"], atol=1e-6)
+
+
+def test_zero_temperature_limit_and_boundedness():
+    rng = np.random.Generator(np.random.Philox(key=12))
+    cold = nb.NmfaParams(alpha=1.0, sigma=0.0, t_f=1)
+    for trial in range(5):
+        n = 25
+        cpl = [(i, j, 1.0 if rng.random() < 0.5 else -1.0) for i in range(n) for j in range(i + 1, n)
+               if rng.random() < 0.5]
+        p = nb.IsingProblem(n, cpl)
+        cfg = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+        phi = nb.mean_field(p, cfg)
+        out = nb.nmfa_step(p, cfg, 1e-6, cold, nb.noise_stream(trial))
+        nz = phi != 0.0
+        assert np.all(np.abs(out[nz] + np.sign(phi[nz])) < 1e-7)   # fp32 state: 1e-9 -> 1e-7
+        assert np.all(np.abs(out) < 1.0)
+    # 20 random-temperature steps keep |s| < 1 strictly (acceptance criterion 2a)
+    p = nb.gen_sk(20, 3)
+    s = np.zeros(p.n)
+    for k in range(20):
+        T = float(np.exp(rng.uniform(np.log(0.02), np.log(2.0))))
+        s = nb.nmfa_step(p, s, T, nb.NmfaParams(alpha=0.9, sigma=0.15, t_f=1), nb.noise_stream(k))
+        assert np.all(np.abs(s) < 1.0)
+
+
+def test_energies_bit_exact_against_reference(G):
+    E = G["energies"]
+    names = sorted({k[:-3] for k in E.files if k.endswith("_ei")})
+    for name in names:
+        p = eprob(G, name)
+        got = nb.energies(p, E[name + "_cfg"].astype(np.float64))
+        if name == "real24_h":
+            assert np.allclose(got, E[name + "_E"], rtol=1e-12, atol=1e-12)
+        else:
+            assert np.array_equal(got, E[name + "_E"]), name
+        if name + "_cut" in E:
+            assert [nb.cut_value(p, c) for c in E[name + "_cfg"][:3]] == list(E[name + "_cut"][:3])
+
+
+@pytest.mark.parametrize("path", ["small", "sparse"])
+def test_replica_sharding_invariance(G, path):
+    p = nb.gen_sk(60, 1) if path == "small" else nb.gen_cubic_maxcut(300, 2)
+    p.device_handle().set_path(path)
+    params = nb.NmfaParams(t_f=200, seed=11)
+    full = nb.sample(p, params, 64, return_s=True)
+    tail = nb.sample(p, params, 32, r0=32, return_s=True)
+    assert torch.equal(full.configs[32:], tail.configs)
+    assert torch.equal(full.energies[32:], tail.energies)
+    assert torch.equal(full.s_final[32:], tail.s_final)
+    # seed + k semantics (solver.py:272): batch(seed=100)[2] == run(seed=102)
+    res = nb.nmfa_batch(p, nb.NmfaParams(t_f=50, seed=100), 5)
+    solo = nb.nmfa_run(p, nb.NmfaParams(t_f=50, seed=102))
+    assert [r.seed for r in res] == [100, 101, 102, 103, 104]
+    assert np.array_equal(res[2].final_config, solo.final_config)
+    assert res[2].final_energy == solo.final_energy
+
+
+def test_returned_energies_match_oracle_energy(G):
+    p = nb.gen_sk(100, 0)
+    op = O.problem_from_edges(100, p.edges_i, p.edges_j, p.edge_weights)
+    res = nb.sample(p, nb.NmfaParams(t_f=300, seed=5), 512)
+    cfg = res.configs.cpu().numpy().astype(np.float64)
+    assert np.array_equal(res.energies.cpu().numpy(), O.energies(op, cfg))
+
+
+def test_best_of_matches_numpy():
+    e = torch.tensor([3.0, -1.0, 2.0, -1.0, -1.0, 5.0], dtype=torch.float64, device="cuda")
+    ss = nb.SampleSet(None, e, 0, 7, 0.0)
+    assert ss.best() == (-1.0, 8)
+    big = torch.randint(-50, 50, (100001,), device="cuda").double()
+    ss = nb.SampleSet(None, big, 0, 0, 0.0)
+    be, bi = ss.best()
+    arr = big.cpu().numpy()
+    assert be == arr.min() and bi == int(np.argmin(arr))
+
+
+def _two_sample_z(k1, n1, k2, n2):
+    p = (k1 + k2) / (n1 + n2)
+    se = np.sqrt(p * (1 - p) * (1 / n1 + 1 / n2))
+    return abs(k1 / n1 - k2 / n2) / se if se > 0 else 0.0
+
+
+def test_success_probability_sk100_consistent_with_reference(G):
+    S = G["stats"]
+    ref = S["sk100_E"]
+    k_ref = int(np.count_nonzero(ref <= -730 + 1e-9))
+    p = nb.gen_sk(100, 0)
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 16384)
+    e = res.energies.cpu().numpy()
+    assert e.min() >= -730.0
+    k = int(np.count_nonzero(e <= -730 + 1e-9))
+    z = _two_sample_z(k, e.size, k_ref, ref.size)
+    lo, hi = nb.wilson_interval(k_ref, ref.size)
+    print(f"sk100 p_gpu={k / e.size:.4f} p_ref={k_ref / ref.size:.4f} ref CI=({lo:.4f},{hi:.4f}) z={z:.2f}")
+    assert z < 4.0
+
+
+@pytest.mark.parametrize("path", ["small", "sparse"])
+def test_success_probability_moebius100_consistent_with_reference(G, path):
+    ref = G["stats"]["moebius100_E"]
+    k_ref = int(np.count_nonzero(ref <= -146 + 1e-9))
+    p = nb.moebius_ladder(100)
+    p.device_handle().set_path(path)
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 8192)
+    e = res.energies.cpu().numpy()
+    assert e.min() >= -146.0
+    k = int(np.count_nonzero(e <= -146 + 1e-9))
+    z = _two_sample_z(k, e.size, k_ref, ref.size)
+    print(f"moebius100[{path}] p_gpu={k / e.size:.4f} p_ref={k_ref / ref.size:.4f} z={z:.2f}")
+    assert z < 4.0
+
+
+def test_moebius16_reaches_ground(G):
+    p = nb.moebius_ladder(16)
+    res = nb.nmfa_batch(p, nb.NmfaParams(t_f=100, seed=0), 100)
+    hits = sum(r.final_energy <= -20.0 + 1e-9 for r in res)
+    assert hits >= 95      # reference: 1000/1000 at t_f=100 (stats.npz)
+    traj = nb.nmfa_run(p, nb.NmfaParams(t_f=100, seed=0), record_trajectory=True).trajectory
+    mag = np.abs(traj.spins).mean(axis=1)
+    assert mag[0] < 0.2 and mag[-1] > 0.8 and mag[-1] > mag[50] > mag[0]
+
+
+def test_g2000_sparse_energy_distribution(G):
+    ref = G["stats"]["g2000_E"]
+    p = nb.gen_dense_maxcut(2000, 0.01, 7)
+    assert p.device_info()["path"] == "sparse"
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 1024)
+    e = res.energies.cpu().numpy()
+    se = np.sqrt(ref.var(ddof=1) / ref.size + e.var(ddof=1) / e.size)
+    print(f"g2000 mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
+          f"min_ref={ref.min()} se={se:.2f}")
+    assert abs(e.mean() - ref.mean()) < 4 * se
+
+
+def test_host_entry_point_matches_device_api():
+    import ctypes
+    p = nb.gen_sk(50, 4)
+    temps = nb.DEFAULT_SCHEDULE.temperatures(100)
+    cfg = np.empty((16, 50), dtype=np.int8)
+    en = np.empty(16)
+    lib = _native.load()
+    _native.check(lib.nmfa_anneal_host(p.device_handle().handle, 16, 100, _native.ptr(temps),
+                                       0.15, 0.15, 9, 0, _native.ptr(cfg), _native.ptr(en)))
+    res = nb.sample(p, nb.NmfaParams(t_f=100, seed=9), 16)
+    assert np.array_equal(cfg, res.configs.cpu().numpy())
+    assert np.array_equal(en, res.energies.cpu().numpy())
+    assert ctypes.c_int64(lib.nmfa_last_launch_count()).value >= 1
