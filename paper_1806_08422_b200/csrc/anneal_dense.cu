@@ -1,25 +1,506 @@
-// Dense large-N NMFA step (tcgen05 GEMM with fused update epilogue).
+// Dense large-N NMFA step: a 2-CTA (cta_group::2) tcgen05 GEMM with the NMFA
+// update fused into its epilogue.  Reference: _kernels_numba.py:71-75
+// (mv = J s; phi = (h + mv)/norm + noise; s = a*(-tanh(phi/T)) + (1-a)*s),
+// batched over replicas.
+//
+// GEMM orientation: D[r, i] = sum_k S[r, k] J[i, k]
+//   M = replicas (256 per CTA pair, 128 per CTA), N = spins (tile of <= 256),
+//   K = spins.  A = S (fp16, K-major), B = J (fp16, K-major; J symmetric).
+// Operand images in HBM are pre-tiled so a (128 rows x 64 k) tile is 16 KB of
+// contiguous bytes in the UMMA canonical no-swizzle K-major layout:
+//   byte(row, k) = (k/64)*Rows*128 + (row/8)*1024 + ((k%64)/8)*128 + (row%8)*16 + (k%8)*2
+// TMA moves them as a 2-D tensor of 128-byte lines.  The epilogue writes the
+// next step's A image directly in that layout (two 16-B stores per 16
+// spins, a warp covers four full 128-B lines), so no transpose pass exists.
+//
+// Roles per CTA (384 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
+// CTA only), warp 2 TMEM allocator, warps 4-11 epilogue (lane quarter x column
+// half).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
+// accumulator slots of 256 columns so the epilogue of tile j overlaps the MMAs
+// of tile j+1.  Each pair owns a contiguous slice of the (replica block,
+// 16-spin unit) space, balanced to within one unit across the 74 pairs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace nmfa {
 
-int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jd) {
-  (void)jd;
-  p->d_j_dense = nullptr;
+constexpr int kDStages = 6;
+constexpr int kDEpiWarps = 8;
+constexpr int kDThreads = 128 + 32 * kDEpiWarps;
+constexpr uint32_t kATile = 128 * 128;
+constexpr uint32_t kBTileMax = 128 * 128;
+constexpr uint32_t kDStageBytes = kATile + kBTileMax;
+constexpr uint32_t kAccCols = 256;
+constexpr size_t kDSmemBytes = (size_t)kDStages * kDStageBytes + 1024;
+
+struct DenseTile {
+  int m_blk, n0, nlen, pad;
+};
+
+struct DenseState {
+  int np = 0, kp = 0, kblocks = 0, k_last_sub = 0, pairs = 0;
+  long long Rp = 0;
+  float* master = nullptr;
+  uint8_t* a_img[2] = {nullptr, nullptr};
+  DenseTile* d_tiles = nullptr;
+  int* d_tile_off = nullptr;
+  CUtensorMap tmA[2];
+  CUtensorMap tmB[5];  // box rows 8, 16, 32, 64, 128
+};
+
+struct DenseStepArgs {
+  const DenseTile* tiles;
+  const int* tile_off;
+  int kblocks, k_last_sub;
+  int n, np;
+  long long R, Rp;
+  int t, t_f;
+  float inv_t, alpha, oma, sigma;
+  const float* invn;
+  const float* hn;
+  float* master;
+  uint8_t* a_next;
+  unsigned long long key_base;
+  const float* noise;
+  int8_t* cfg;
+  float* s_out;
+  float* s_hist;
+  int last;
+};
+
+// ---------------------------------------------------------------------------
+// cluster / 2-CTA PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                           uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(mbar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_remote_arrive(uint32_t mbar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
+    dense_step_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB8,
+                      const __grid_constant__ CUtensorMap tmB16,
+                      const __grid_constant__ CUtensorMap tmB32,
+                      const __grid_constant__ CUtensorMap tmB64,
+                      const __grid_constant__ CUtensorMap tmB128, const DenseStepArgs a) {
+  extern __shared__ __align__(1024) uint8_t dsmem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kDStages], empty_bar[kDStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int j0 = a.tile_off[pair], j1 = a.tile_off[pair + 1];
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kDStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * kDEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(&tmem_slot, 2 * kAccCols);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tbase = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------- TMA producer -------------------------
+    if (lane == 0) {
+      const CUtensorMap* tmB[5] = {&tmB8, &tmB16, &tmB32, &tmB64, &tmB128};
+      int it = 0;
+      for (int j = j0; j < j1; ++j) {
+        const DenseTile tl = a.tiles[j];
+        const int half = tl.nlen >> 1;
+        const int arow = tl.m_blk * 256 + (int)cta * 128;
+        const int brow = tl.n0 + (int)cta * half;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const int s = it % kDStages;
+          mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+          const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
+          if (cta == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * 128u));
+          uint8_t* st = smem + (size_t)s * kDStageBytes;
+          tma2d_pair(smem_u32(st), &tmA, 0, (int)(kb * a.Rp) + arow, fb);
+          int off = 0;
+#pragma unroll
+          for (int b = 4; b >= 0; --b) {
+            const int rows = 8 << b;
+            if (half & rows) {
+              tma2d_pair(smem_u32(st + kATile + off * 128), tmB[b], 0, kb * a.np + brow + off, fb);
+              off += rows;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------- MMA issuer (leader CTA) -------------------------
+    if (cta == 0 && lane == 0) {
+      int it = 0;
+      for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
+        const DenseTile tl = a.tiles[j];
+        const int slot = jj & 1, use = jj >> 1;
+        mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
+        const uint32_t d = tbase + (uint32_t)slot * kAccCols;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const int s = it % kDStages;
+          mbar_wait(&full_bar[s], (it / kDStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + (size_t)s * kDStageBytes);
+          const uint32_t sb = sa + kATile;
+          const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : 4;
+          for (int ks = 0; ks < nsub; ++ks) {
+            mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 1024),
+                     make_desc_noswizzle(sb + ks * 256, 128, 1024), idesc, (kb | ks) ? 1u : 0u);
+          }
+          commit_pair_mc(&empty_bar[s]);
+        }
+        commit_pair_mc(&tfull_bar[slot]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------- fused NMFA epilogue -------------------------
+    const int e = warp - 4, quarter = e & 3, hpart = e >> 2;
+    const int row = 32 * quarter + lane;
+    const uint32_t leader_tempty[2] = {map_to_rank(smem_u32(&tempty_bar[0]), 0),
+                                       map_to_rank(smem_u32(&tempty_bar[1]), 0)};
+    float4* master4 = reinterpret_cast<float4*>(a.master);
+    for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
+      const DenseTile tl = a.tiles[j];
+      const int slot = jj & 1, use = jj >> 1;
+      const long long r = (long long)tl.m_blk * 256 + (long long)cta * 128 + row;
+      const bool valid = r < a.R;
+      const unsigned long long key = a.key_base + (unsigned long long)r;
+      const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+      mbar_wait(&tfull_bar[slot], use & 1);
+      tc_fence_after();
+      const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
+      const int nch = tl.nlen >> 4;
+      for (int c = hpart; c < nch; c += 2) {
+        const int i0 = tl.n0 + 16 * c;
+        float acc[16];
+        tmem_ld16(tacc + 16 * c, acc);
+        tmem_wait_ld();
+        if (i0 >= a.n) continue;
+        float ms[16], z[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 m = master4[(long long)(i0 / 4 + q) * a.Rp + r];
+          ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
+        }
+        if (a.noise) {
+          const float* nz = a.noise + ((long long)r * a.t_f + a.t) * a.n;
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) z[cc] = (valid && i0 + cc < a.n) ? nz[i0 + cc] : 0.f;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) normal4(k0, k1, (uint32_t)(i0 / 4 + q), (uint32_t)a.t, &z[4 * q]);
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) z[cc] *= a.sigma;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const int i = i0 + cc;
+          ms[cc] = (i < a.n) ? nmfa_update(acc[cc], __ldg(a.invn + i), __ldg(a.hn + i), z[cc],
+                                           a.inv_t, a.alpha, a.oma, ms[cc])
+                             : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          master4[(long long)(i0 / 4 + q) * a.Rp + r] =
+              make_float4(ms[4 * q], ms[4 * q + 1], ms[4 * q + 2], ms[4 * q + 3]);
+        // next step's A operand image (pre-tiled K-major, see header)
+        uint8_t* img = a.a_next + (long long)(i0 >> 6) * a.Rp * 128 + (r >> 3) * 1024 +
+                       ((i0 & 63) >> 3) * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4*>(img) =
+            make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
+                       pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
+        *reinterpret_cast<uint4*>(img + 128) =
+            make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
+                       pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
+        if (valid) {
+          if (a.s_hist) {
+            float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n;
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc)
+              if (i0 + cc < a.n) hrow[i0 + cc] = ms[cc];
+          }
+          if (a.last) {
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+              const int i = i0 + cc;
+              if (i < a.n) {
+                a.cfg[r * a.n + i] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;
+                if (a.s_out) a.s_out[r * a.n + i] = ms[cc];
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_remote_arrive(leader_tempty[slot]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, 2 * kAccCols);
+  }
+}
+
+// master[i/4][r][i%4] and A image 0 from s0 (or zeros)
+__global__ void dense_init_kernel(float* master, uint8_t* a_img, const float* s0, int n, int np,
+                                  int kp, long long R, long long Rp) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)kp * Rp) return;
+  const long long r = e % Rp;
+  const int i = (int)(e / Rp);
+  const float v = (s0 && r < R && i < n) ? s0[r * n + i] : 0.f;
+  if (i < np) master[((long long)(i >> 2) * Rp + r) * 4 + (i & 3)] = v;
+  const long long off = (long long)(i >> 6) * Rp * 128 + (r >> 3) * 1024 + ((i & 63) >> 3) * 128 +
+                        (r & 7) * 16 + (i & 7) * 2;
+  *reinterpret_cast<__half*>(a_img + off) = __float2half_rn(v);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_line_map(CUtensorMap* tm, void* base, uint64_t lines, uint32_t box_lines) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return NMFA_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {64, lines};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, box_lines};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return NMFA_ERR_CUDA;
+  }
   return NMFA_OK;
 }
 
+static inline size_t img_off(uint32_t row, uint32_t k, uint32_t rows) {
+  return (size_t)(k >> 6) * rows * 128 + (row >> 3) * 1024 + ((k & 63) >> 3) * 128 + (row & 7) * 16 +
+         (k & 7) * 2;
+}
+
+int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jd) {
+  const uint32_t n = (uint32_t)p->n;
+  const uint32_t np = (n + 15) / 16 * 16, kp = (n + 63) / 64 * 64;
+  std::vector<__half> img((size_t)kp * np, __float2half(0.f));
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t k = 0; k < n; ++k) {
+      const float v = jd[(size_t)i * n + k];
+      if (v != 0.f) img[img_off(i, k, np) / 2] = __float2half(v);
+    }
+  p->j_dense_bytes = img.size() * 2;
+  NMFA_CUDA_TRY(cudaMalloc(&p->d_j_dense, p->j_dense_bytes));
+  NMFA_CUDA_TRY(cudaMemcpy(p->d_j_dense, img.data(), p->j_dense_bytes, cudaMemcpyHostToDevice));
+  return NMFA_OK;
+}
+
+void dense_plan_free(nmfa_plan* pl) {
+  auto* ds = static_cast<DenseState*>(pl->dense);
+  if (!ds) return;
+  if (ds->master) cudaFree(ds->master);
+  if (ds->a_img[0]) cudaFree(ds->a_img[0]);
+  if (ds->a_img[1]) cudaFree(ds->a_img[1]);
+  if (ds->d_tiles) cudaFree(ds->d_tiles);
+  if (ds->d_tile_off) cudaFree(ds->d_tile_off);
+  delete ds;
+  pl->dense = nullptr;
+}
+
 int dense_plan_alloc(nmfa_plan* pl) {
-  (void)pl;
+  const nmfa_problem* p = pl->p;
+  auto* ds = new DenseState();
+  pl->dense = ds;
+  const int n = (int)p->n;
+  ds->np = (n + 15) / 16 * 16;
+  ds->kp = (n + 63) / 64 * 64;
+  ds->kblocks = ds->kp / 64;
+  ds->k_last_sub = (n - (ds->kblocks - 1) * 64 + 15) / 16;
+  ds->Rp = (pl->R + 255) / 256 * 256;
+  const size_t master_bytes = (size_t)(ds->np / 4) * ds->Rp * 16;
+  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  NMFA_CUDA_TRY(cudaMalloc(&ds->master, master_bytes));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[0], img_bytes));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[1], img_bytes));
+  NMFA_CUDA_TRY(cudaMemset(ds->a_img[0], 0, img_bytes));
+  NMFA_CUDA_TRY(cudaMemset(ds->a_img[1], 0, img_bytes));
+
+  // balanced static schedule over (replica block, 16-spin unit)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const long long upm = ds->np / 16, mb = ds->Rp / 256, U = upm * mb;
+  const int pairs = (int)std::min<long long>(sms / 2, U);
+  ds->pairs = pairs;
+  std::vector<DenseTile> tiles;
+  std::vector<int> off(pairs + 1, 0);
+  for (int q = 0; q < pairs; ++q) {
+    long long u = U * q / pairs;
+    const long long u1 = U * (q + 1) / pairs;
+    while (u < u1) {
+      const long long m = u / upm;
+      const long long seg_end = std::min(u1, (m + 1) * upm);
+      const long long L = seg_end - u, nt = (L + 15) / 16;
+      for (long long k = 0; k < nt; ++k) {
+        const long long a0 = L * k / nt, a1 = L * (k + 1) / nt;
+        tiles.push_back({(int)m, (int)((u - m * upm + a0) * 16), (int)((a1 - a0) * 16), 0});
+      }
+      u = seg_end;
+    }
+    off[q + 1] = (int)tiles.size();
+  }
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_tiles, tiles.size() * sizeof(DenseTile)));
+  NMFA_CUDA_TRY(cudaMemcpy(ds->d_tiles, tiles.data(), tiles.size() * sizeof(DenseTile),
+                           cudaMemcpyHostToDevice));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_tile_off, off.size() * sizeof(int)));
+  NMFA_CUDA_TRY(
+      cudaMemcpy(ds->d_tile_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+
+  int err;
+  for (int b = 0; b < 2; ++b)
+    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp, 128)))
+      return err;
+  for (int b = 0; b < 5; ++b)
+    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np, 8u << b)))
+      return err;
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kDSmemBytes));
   return NMFA_OK;
 }
 
 int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         cudaStream_t st) {
-  // Until the tcgen05 dense kernel lands, dense problems run the CSR path.
-  return launch_sparse_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
+  const nmfa_problem* p = pl->p;
+  auto* ds = static_cast<DenseState*>(pl->dense);
+  if (!ds) {
+    set_error("dense plan state missing");
+    return NMFA_ERR_STATE;
+  }
+  const long long tot = (long long)ds->kp * ds->Rp;
+  dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      ds->master, ds->a_img[0], s0, (int)p->n, ds->np, ds->kp, pl->R, ds->Rp);
+  NMFA_LAUNCH_CHECK();
+  DenseStepArgs a{};
+  a.tiles = ds->d_tiles;
+  a.tile_off = ds->d_tile_off;
+  a.kblocks = ds->kblocks;
+  a.k_last_sub = ds->k_last_sub;
+  a.n = (int)p->n;
+  a.np = ds->np;
+  a.R = pl->R;
+  a.Rp = ds->Rp;
+  a.t_f = pl->t_f;
+  a.alpha = pl->alpha;
+  a.oma = pl->oma;
+  a.sigma = pl->sigma;
+  a.invn = p->d_invn;
+  a.hn = p->d_hn;
+  a.master = ds->master;
+  a.key_base = key_base;
+  a.noise = noise;
+  a.cfg = cfg;
+  a.s_out = s_out;
+  a.s_hist = s_hist;
+  for (int t = 0; t < pl->t_f; ++t) {
+    a.t = t;
+    a.inv_t = pl->h_inv_temp[t];
+    a.last = (t == pl->t_f - 1);
+    a.a_next = ds->a_img[(t + 1) & 1];
+    dense_step_kernel<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
+        ds->tmA[t & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
+    NMFA_LAUNCH_CHECK();
+  }
+  add_launches(1 + pl->t_f);
+  return NMFA_OK;
 }
 
 }  // namespace nmfa

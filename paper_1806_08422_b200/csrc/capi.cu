@@ -308,6 +308,7 @@ int nmfa_plan_destroy(nmfa_plan_t* pl) {
                   pl->d_h16b,     pl->d_bits,  pl->d_epart,    pl->d_hist_cfg};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  dense_plan_free(pl);
   cudaSetDevice(prev);
   delete pl;
   return NMFA_OK;

@@ -81,6 +81,7 @@ struct nmfa_plan {
   int64_t energy_chunks = 0;
   int8_t* d_hist_cfg = nullptr; // trajectory energies: signs of s_hist
   int64_t bits_words = 0;       // capacity of d_bits in uint32
+  void* dense = nullptr;        // DenseState (anneal_dense.cu)
 };
 
 namespace nmfa {
@@ -95,6 +96,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         cudaStream_t st);
 int dense_plan_alloc(nmfa_plan* pl);
+void dense_plan_free(nmfa_plan* pl);
 int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jdense_rowmajor);
 int launch_energy(const nmfa_problem* p, const int8_t* cfg, int64_t n_cfg, double* energy,
                   uint32_t* bits_scratch, double* part_scratch, int64_t chunks,

@@ -51,8 +51,11 @@ def assert_traj_close(s_gpu, s_ref, tol=2e-2):
     assert np.array_equal(np.sign(s_gpu[firm]), np.sign(s_ref[firm]))
 
 
+PATHS = ["small", "sparse", "dense"]
+
+
 @pytest.mark.parametrize("name", TRAJ)
-@pytest.mark.parametrize("path", ["small", "sparse"])
+@pytest.mark.parametrize("path", PATHS)
 def test_injected_noise_trajectory_matches_reference(G, name, path):
     T = G["trajectories"]
     p = eprob(G, name)
@@ -77,7 +80,7 @@ def test_injected_noise_trajectory_matches_reference(G, name, path):
 
 
 @pytest.mark.parametrize("name", ["moebius16", "cubic40_s1", "sk30_s2", "sk100_s0"])
-@pytest.mark.parametrize("path", ["small", "sparse"])
+@pytest.mark.parametrize("path", PATHS)
 def test_noise_negation_is_exact(G, name, path):
     p = eprob(G, name)
     p.device_handle().set_path(path)
@@ -166,9 +169,10 @@ def test_energies_bit_exact_against_reference(G):
             assert [nb.cut_value(p, c) for c in E[name + "_cfg"][:3]] == list(E[name + "_cut"][:3])
 
 
-@pytest.mark.parametrize("path", ["small", "sparse"])
+@pytest.mark.parametrize("path", PATHS)
 def test_replica_sharding_invariance(G, path):
-    p = nb.gen_sk(60, 1) if path == "small" else nb.gen_cubic_maxcut(300, 2)
+    p = {"small": lambda: nb.gen_sk(60, 1), "sparse": lambda: nb.gen_cubic_maxcut(300, 2),
+         "dense": lambda: nb.gen_sk(300, 2)}[path]()
     p.device_handle().set_path(path)
     params = nb.NmfaParams(t_f=200, seed=11)
     full = nb.sample(p, params, 64, return_s=True)
@@ -274,3 +278,35 @@ def test_host_entry_point_matches_device_api():
     assert np.array_equal(cfg, res.configs.cpu().numpy())
     assert np.array_equal(en, res.energies.cpu().numpy())
     assert ctypes.c_int64(lib.nmfa_last_launch_count()).value >= 1
+
+
+def test_dense_large_injected_noise_matches_oracle():
+    """n = 520 (not a multiple of 16/64), several replica blocks, dense tcgen05 path."""
+    p = nb.gen_sk(520, 5)
+    assert p.device_info()["path"] == "dense"
+    op = O.problem_from_edges(520, p.edges_i, p.edges_j, p.edge_weights)
+    t_f, R = 120, 300
+    temps = O.temperatures(t_f)
+    rng = np.random.Generator(np.random.Philox(key=99))
+    noise = rng.standard_normal((R, t_f, p.n)) * 0.15
+    S, _ = nb.run_with_noise(p, temps, noise, 0.15)
+    Sref = O.batched_anneal(op, None, t_f=t_f, temps=temps, noise=noise)
+    err = np.abs(S - Sref)
+    assert np.mean(err) < 1e-3 and np.quantile(err, 0.999) < 2e-2, (np.mean(err), err.max())
+    flips = np.mean(np.sign(S) != np.sign(Sref))
+    assert flips < 2e-3, flips
+
+
+def test_k2000_standin_energy_distribution(G):
+    ref = G["stats"]["sk2000_E"]
+    p = nb.gen_sk(2000, 7)
+    assert p.device_info()["path"] == "dense"
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 1024)
+    e = res.energies.cpu().numpy()
+    op = O.problem_from_edges(2000, p.edges_i, p.edges_j, p.edge_weights)
+    cfg = res.configs[:64].cpu().numpy().astype(np.float64)
+    assert np.array_equal(e[:64], O.energies(op, cfg))
+    se = np.sqrt(ref.var(ddof=1) / ref.size + e.var(ddof=1) / e.size)
+    print(f"k2000 mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
+          f"min_ref={ref.min()} se={se:.2f}")
+    assert abs(e.mean() - ref.mean()) < 4 * se
