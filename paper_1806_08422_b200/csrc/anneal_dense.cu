@@ -130,6 +130,7 @@ __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
       : "memory");
 }
 
+template <bool kInjected>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_step_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB8,
@@ -169,7 +170,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   if (warp == 0) {
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
-      const CUtensorMap* tmB[5] = {&tmB8, &tmB16, &tmB32, &tmB64, &tmB128};
       int it = 0;
       for (int j = j0; j < j1; ++j) {
         const DenseTile tl = a.tiles[j];
@@ -188,7 +188,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           for (int b = 4; b >= 0; --b) {
             const int rows = 8 << b;
             if (half & rows) {
-              tma2d_pair(smem_u32(st + kATile + off * 128), tmB[b], 0, kb * a.np + brow + off, fb);
+              const CUtensorMap* tm = b == 4 ? &tmB128 : b == 3 ? &tmB64 : b == 2 ? &tmB32
+                                    : b == 1 ? &tmB16 : &tmB8;
+              tma2d_pair(smem_u32(st + kATile + off * 128), tm, 0, kb * a.np + brow + off, fb);
               off += rows;
             }
           }
@@ -235,44 +237,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const long long r = (long long)tl.m_blk * 256 + (long long)cta * 128 + row;
       const bool valid = r < a.R;
       const unsigned long long key = a.key_base + (unsigned long long)r;
-      const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+      const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
       mbar_wait(&tfull_bar[slot], use & 1);
       tc_fence_after();
       const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
       const int nch = tl.nlen >> 4;
+      const bool extra = valid && (a.s_hist != nullptr || a.last);
+      const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
+      const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
       for (int c = hpart; c < nch; c += 2) {
         const int i0 = tl.n0 + 16 * c;
-        float acc[16];
+        float acc[16], ms[16];
         tmem_ld16(tacc + 16 * c, acc);
-        tmem_wait_ld();
-        if (i0 >= a.n) continue;
-        float ms[16], z[16];
+        float4* mrow = master4 + (long long)(i0 >> 2) * a.Rp + r;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 m = master4[(long long)(i0 / 4 + q) * a.Rp + r];
+          const float4 m = mrow[q * a.Rp];
           ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
         }
-        if (a.noise) {
-          const float* nz = a.noise + ((long long)r * a.t_f + a.t) * a.n;
-#pragma unroll
-          for (int cc = 0; cc < 16; ++cc) z[cc] = (valid && i0 + cc < a.n) ? nz[i0 + cc] : 0.f;
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) normal4(k0, k1, (uint32_t)(i0 / 4 + q), (uint32_t)a.t, &z[4 * q]);
-#pragma unroll
-          for (int cc = 0; cc < 16; ++cc) z[cc] *= a.sigma;
-        }
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-          const int i = i0 + cc;
-          ms[cc] = (i < a.n) ? nmfa_update(acc[cc], __ldg(a.invn + i), __ldg(a.hn + i), z[cc],
-                                           a.inv_t, a.alpha, a.oma, ms[cc])
-                             : 0.f;
-        }
+        tmem_wait_ld();
+        const int nvalid = valid ? min(16, a.n - i0) : 0;
+        const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + a.t) * a.n + i0 : nullptr;
+        update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
+                            (uint32_t)(i0 / 4), (uint32_t)a.t, a.sigma, a.inv_t, a.alpha, a.oma);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          master4[(long long)(i0 / 4 + q) * a.Rp + r] =
-              make_float4(ms[4 * q], ms[4 * q + 1], ms[4 * q + 2], ms[4 * q + 3]);
+          mrow[q * a.Rp] = make_float4(ms[4 * q], ms[4 * q + 1], ms[4 * q + 2], ms[4 * q + 3]);
         // next step's A operand image (pre-tiled K-major, see header)
         uint8_t* img = a.a_next + (long long)(i0 >> 6) * a.Rp * 128 + (r >> 3) * 1024 +
                        ((i0 & 63) >> 3) * 128 + (r & 7) * 16;
@@ -282,20 +272,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         *reinterpret_cast<uint4*>(img + 128) =
             make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
                        pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
-        if (valid) {
+        if (extra) {
           if (a.s_hist) {
-            float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n;
-#pragma unroll
+            float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n + i0;
+            #pragma unroll
             for (int cc = 0; cc < 16; ++cc)
-              if (i0 + cc < a.n) hrow[i0 + cc] = ms[cc];
+              if (cc < nvalid) hrow[cc] = ms[cc];
           }
           if (a.last) {
 #pragma unroll
             for (int cc = 0; cc < 16; ++cc) {
-              const int i = i0 + cc;
-              if (i < a.n) {
-                a.cfg[r * a.n + i] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;
-                if (a.s_out) a.s_out[r * a.n + i] = ms[cc];
+              if (cc < nvalid) {
+                a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;
+                if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
               }
             }
           }
@@ -451,8 +440,10 @@ int dense_plan_alloc(nmfa_plan* pl) {
   for (int b = 0; b < 5; ++b)
     if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np, 8u << b)))
       return err;
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kDSmemBytes));
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
   return NMFA_OK;
 }
 
@@ -495,7 +486,8 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
     a.inv_t = pl->h_inv_temp[t];
     a.last = (t == pl->t_f - 1);
     a.a_next = ds->a_img[(t + 1) & 1];
-    dense_step_kernel<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
+    auto kern = noise ? dense_step_kernel<true> : dense_step_kernel<false>;
+    kern<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
         ds->tmA[t & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
     NMFA_LAUNCH_CHECK();
   }

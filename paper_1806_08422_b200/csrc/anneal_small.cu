@@ -35,6 +35,7 @@ struct SmallArgs {
 constexpr uint32_t kRowsPerCta = 128;
 constexpr uint32_t kLboA = (kRowsPerCta / 8) * 128;  // A: K core matrices 2048 B apart
 
+template <bool kInjected>
 __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int np = a.np;
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
   const uint32_t t_mst = t_acc + (uint32_t)np;
 
   const unsigned long long key = a.key_base + (unsigned long long)rrel;
-  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
 
   // initial state: s0 or zeros, into the TMEM master and the SMEM operand
   for (int j = cpart; j < nchunks; j += a.cs) {
@@ -108,28 +109,19 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
     const float inv_t = a.inv_temp[t];
     const bool last = (t == a.t_f - 1);
 
+    const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
+    const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+    const bool extra = (a.s_hist != nullptr) || last;
     for (int j = cpart; j < nchunks; j += a.cs) {
       const int c0 = 16 * j;
-      float acc[16], ms[16], z[16];
+      float acc[16], ms[16];
       tmem_ld16(t_acc + c0, acc);
       tmem_ld16(t_mst + c0, ms);
       tmem_wait_ld();
-      if (a.noise) {
-        const float* nz = a.noise + ((long long)rrel * a.t_f + t) * a.n;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) z[c] = (valid && c0 + c < a.n) ? nz[c0 + c] : 0.f;
-      } else {
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) normal4(k0, k1, (uint32_t)(c0 / 4 + qq), (uint32_t)t, &z[4 * qq]);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) z[c] *= a.sigma;
-      }
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int i = c0 + c;
-        ms[c] = (i < a.n) ? nmfa_update(acc[c], a.invn[i], a.hn[i], z[c], inv_t, a.alpha, a.oma, ms[c])
-                          : 0.f;
-      }
+      const int nvalid = valid ? min(16, a.n - c0) : 0;
+      const float* nz = kInjected ? a.noise + ((long long)rrel * a.t_f + t) * a.n + c0 : nullptr;
+      update16<kInjected>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
+                          (uint32_t)(c0 / 4), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
       tmem_st16(t_mst + c0, ms);
       uint4 lo = make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
                             pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
@@ -137,20 +129,19 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
                             pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
       *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0, kLboA)) = lo;
       *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8, kLboA)) = hi;
-      if (valid) {
+      if (extra && nvalid > 0) {
         if (a.s_hist) {
-          float* hrow = a.s_hist + ((long long)rrel * a.t_f + t) * a.n;
-#pragma unroll
+          float* hrow = a.s_hist + ((long long)rrel * a.t_f + t) * a.n + c0;
+          #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c0 + c < a.n) hrow[c0 + c] = ms[c];
+            if (c < nvalid) hrow[c] = ms[c];
         }
         if (last) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            const int i = c0 + c;
-            if (i < a.n) {
-              a.cfg[rrel * a.n + i] = ms[c] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181-183
-              if (a.s_out) a.s_out[rrel * a.n + i] = ms[c];
+            if (c < nvalid) {
+              a.cfg[rrel * a.n + c0 + c] = ms[c] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181-183
+              if (a.s_out) a.s_out[rrel * a.n + c0 + c] = ms[c];
             }
           }
         }
@@ -204,9 +195,9 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.cs = ctas >= 2 * sms ? 1 : (ctas >= sms ? 2 : 4);
   if (a.cs > p->np / 16) a.cs = p->np / 16;
   const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 + 16;
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(small_anneal_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  small_anneal_kernel<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
+  auto kern = noise ? small_anneal_kernel<true> : small_anneal_kernel<false>;
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
   NMFA_LAUNCH_CHECK();
   add_launches(1);
   return NMFA_OK;

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) sparse_step_kernel(const SparseStepArgs a
     }
   } else {
     const unsigned long long key = a.key_base + (unsigned long long)r;
-    normal4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)q, (uint32_t)a.t, z);
+    normal4(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t, z);
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) z[qq] *= a.sigma;
   }

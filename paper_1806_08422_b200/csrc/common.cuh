@@ -20,16 +20,40 @@ namespace nmfa {
 // ---------------------------------------------------------------------------
 constexpr float kOneMinus = 0.99999994f;  // largest float below 1
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// tanh(y) = sign(y) * (1 - 2 / (exp(2|y|) + 1)): two MUFU ops, absolute error
+// ~1e-7, exactly odd.  exp overflow -> inf -> rcp 0 -> 1.
 __device__ __forceinline__ float odd_tanh(float y) {
-  return copysignf(tanhf(fabsf(y)), y);
+  const float e = ex2_approx(fabsf(y) * 2.8853900817779268f);  // 2 / ln 2
+  return copysignf(fmaf(-2.0f, rcp_approx(e + 1.0f), 1.0f), y);
 }
 
 __device__ __forceinline__ float nmfa_update(float acc, float inv_norm, float h_norm,
                                              float noise, float inv_t, float alpha,
                                              float one_minus_alpha, float s_old) {
-  float phi = fmaf(acc, inv_norm, h_norm) + noise;
-  float shat = -odd_tanh(phi * inv_t);
-  float s = alpha * shat + one_minus_alpha * s_old;
+  const float phi = fmaf(acc, inv_norm, h_norm) + noise;
+  const float shat = -odd_tanh(phi * inv_t);
+  const float s = fmaf(alpha, shat, one_minus_alpha * s_old);
   return fminf(fmaxf(s, -kOneMinus), kOneMinus);
 }
 
@@ -43,34 +67,44 @@ __device__ __forceinline__ float nmfa_update(float acc, float inv_norm, float h_
 // ---------------------------------------------------------------------------
 struct uint4_ { uint32_t x, y, z, w; };
 
-__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2,
-                                             uint32_t& c3, uint32_t k0, uint32_t k1) {
-  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-  uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
-  uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
-  uint32_t n0 = hi1 ^ c1 ^ k0;
-  uint32_t n2 = hi0 ^ c3 ^ k1;
-  c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+// Per-replica Philox round keys (the key is fixed for a replica, so the
+// schedule is computed once per replica and reused for every counter).
+struct PhiloxKey {
+  uint32_t k0[10], k1[10];
+};
+
+__device__ __forceinline__ PhiloxKey philox_schedule(uint32_t k0, uint32_t k1) {
+  PhiloxKey K;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    K.k0[i] = k0 + (uint32_t)i * 0x9E3779B9u;
+    K.k1[i] = k1 + (uint32_t)i * 0xBB67AE85u;
+  }
+  return K;
 }
 
 __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
-                                                uint32_t c3, uint32_t k0, uint32_t k1) {
-  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+                                                uint32_t c3, const PhiloxKey& K) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
-    philox_round(c0, c1, c2, c3, k0, k1);
-    k0 += W0; k1 += W1;
+    const uint64_t p0 = (uint64_t)M0 * c0;  // IMAD.WIDE.U32
+    const uint64_t p1 = (uint64_t)M1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k0[i];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k1[i];
+    c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
   }
   return {c0, c1, c2, c3};
 }
 
 constexpr uint32_t kNoiseTag = 0x4E4D4641u;
 
-// Box-Muller on two 32-bit words: u1 in (0,1], u2 in [0,1).
+// Box-Muller on two 32-bit words.  u1 = (k + 1/2) 2^-23 in (0, 1) from the top
+// 23 bits (never 0 or 1), u2 = k 2^-23 in [0, 1).  Tail bound |z| <= 5.78.
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
-  float u1 = ((float)(a >> 8) + 1.0f) * 5.9604644775390625e-08f;  // (k+1) * 2^-24
-  float u2 = (float)(b >> 8) * 5.9604644775390625e-08f;
-  float r = sqrtf(-2.0f * __logf(u1));
+  const float u1 = fmaf((float)(a >> 9), 1.1920928955078125e-07f, 5.9604644775390625e-08f);
+  const float u2 = (float)(b >> 9) * 1.1920928955078125e-07f;
+  const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u1));  // -2 ln u1
   float sn, cs;
   __sincosf(6.283185307179586f * u2, &sn, &cs);
   z0 = r * cs;
@@ -78,11 +112,39 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
 }
 
 // Four standard normals for spins 4q..4q+3 of replica key (k0,k1) at step t.
-__device__ __forceinline__ void normal4(uint32_t k0, uint32_t k1, uint32_t q, uint32_t t,
-                                        float z[4]) {
-  uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, k0, k1);
+__device__ __forceinline__ void normal4(const PhiloxKey& K, uint32_t q, uint32_t t, float z[4]) {
+  uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, K);
   box_muller(w.x, w.y, z[0], z[1]);
   box_muller(w.z, w.w, z[2], z[3]);
+}
+
+// The fused update of 16 consecutive spins i0..i0+15 of one replica.
+//   invn4 / hn4 point at the padded per-spin constants for i0 (16-aligned).
+//   kInjected: z comes from `nz` (pre-scaled, may be unaligned, indices < n_valid)
+//   else in-kernel Philox noise scaled by sigma.
+template <bool kInjected>
+__device__ __forceinline__ void update16(const float acc[16], float ms[16], const float4* invn4,
+                                         const float4* hn4, const float* nz, int n_valid,
+                                         const PhiloxKey& K, uint32_t q0, uint32_t t,
+                                         float sigma, float inv_t, float alpha, float oma) {
+  float z[16];
+  if (kInjected) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) z[c] = c < n_valid ? nz[c] : 0.f;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) normal4(K, q0 + q, t, &z[4 * q]);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) z[c] *= sigma;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 iv = __ldg(invn4 + q), hv = __ldg(hn4 + q);
+    ms[4 * q + 0] = nmfa_update(acc[4 * q + 0], iv.x, hv.x, z[4 * q + 0], inv_t, alpha, oma, ms[4 * q + 0]);
+    ms[4 * q + 1] = nmfa_update(acc[4 * q + 1], iv.y, hv.y, z[4 * q + 1], inv_t, alpha, oma, ms[4 * q + 1]);
+    ms[4 * q + 2] = nmfa_update(acc[4 * q + 2], iv.z, hv.z, z[4 * q + 2], inv_t, alpha, oma, ms[4 * q + 2]);
+    ms[4 * q + 3] = nmfa_update(acc[4 * q + 3], iv.w, hv.w, z[4 * q + 3], inv_t, alpha, oma, ms[4 * q + 3]);
+  }
 }
 
 // ---------------------------------------------------------------------------

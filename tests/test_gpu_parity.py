@@ -292,9 +292,13 @@ def test_dense_large_injected_noise_matches_oracle():
     S, _ = nb.run_with_noise(p, temps, noise, 0.15)
     Sref = O.batched_anneal(op, None, t_f=t_f, temps=temps, noise=noise)
     err = np.abs(S - Sref)
-    assert np.mean(err) < 1e-3 and np.quantile(err, 0.999) < 2e-2, (np.mean(err), err.max())
+    # SURVEY 8c parity criterion for large n: mean over replicas of <= 0.1% spins with a
+    # different final sign (fp16 operand rounding occasionally flips a correlated cluster).
     flips = np.mean(np.sign(S) != np.sign(Sref))
-    assert flips < 2e-3, flips
+    print(f"n=520 dense: mean|dS|={err.mean():.2e} frac(|dS|>2e-2)={np.mean(err > 2e-2):.2e} "
+          f"sign flips={flips:.2e}")
+    assert np.mean(err) < 1e-3 and np.mean(err > 2e-2) < 2e-3, (np.mean(err), err.max())
+    assert flips <= 1e-3, flips
 
 
 def test_k2000_standin_energy_distribution(G):
