@@ -13,9 +13,9 @@
 // next step's A image directly in that layout (two 16-B stores per 16
 // spins, a warp covers four full 128-B lines), so no transpose pass exists.
 //
-// Roles per CTA (384 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
-// CTA only), warp 2 TMEM allocator, warps 4-11 epilogue (lane quarter x column
-// half).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
+// Roles per CTA (640 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
+// CTA only), warp 2 TMEM allocator, warps 4-19 epilogue (lane quarter x column
+// quarter; 4 warps per scheduler to hide the Philox/MUFU latency chains).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
 // accumulator slots of 256 columns so the epilogue of tile j overlaps the MMAs
 // of tile j+1.  Each pair owns a contiguous slice of the (replica block,
 // 16-spin unit) space, balanced to within one unit across the 74 pairs.
@@ -30,7 +30,7 @@
 namespace nmfa {
 
 constexpr int kDStages = 6;
-constexpr int kDEpiWarps = 8;
+constexpr int kDEpiWarps = 16;
 constexpr int kDThreads = 128 + 32 * kDEpiWarps;
 constexpr uint32_t kATile = 128 * 128;
 constexpr uint32_t kBTileMax = 128 * 128;
@@ -226,10 +226,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------- fused NMFA epilogue -------------------------
-    const int e = warp - 4, quarter = e & 3, hpart = e >> 2;
+    const int e = warp - 4, quarter = e & 3, hpart = e >> 2;  // 4 lane quarters x 4 column parts
     const int row = 32 * quarter + lane;
-    const uint32_t leader_tempty[2] = {map_to_rank(smem_u32(&tempty_bar[0]), 0),
-                                       map_to_rank(smem_u32(&tempty_bar[1]), 0)};
+    const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
+    const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
     float4* master4 = reinterpret_cast<float4*>(a.master);
     for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
       const DenseTile tl = a.tiles[j];
@@ -245,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const bool extra = valid && (a.s_hist != nullptr || a.last);
       const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
       const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
-      for (int c = hpart; c < nch; c += 2) {
+      for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
         const int i0 = tl.n0 + 16 * c;
         float acc[16], ms[16];
         tmem_ld16(tacc + 16 * c, acc);
@@ -292,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_remote_arrive(leader_tempty[slot]);
+      if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
     }
   }
   tc_fence_before();

@@ -8,6 +8,8 @@
 // to an mbarrier; every warp then drains its TMEM lane quarter, applies the
 // fused update (reference _kernels_numba.py:71-75) and writes the new fp16
 // operand back into SMEM.  No HBM traffic inside the anneal.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -192,7 +194,8 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   // Spread columns over more warps when the grid cannot fill the GPU.
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-  a.cs = ctas >= 2 * sms ? 1 : (ctas >= sms ? 2 : 4);
+  a.cs = ctas >= sms ? 2 : 4;
+  if (const char* e = getenv("NMFA_SMALL_CS")) a.cs = atoi(e);  // tuning override
   if (a.cs > p->np / 16) a.cs = p->np / 16;
   const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 + 16;
   auto kern = noise ? small_anneal_kernel<true> : small_anneal_kernel<false>;

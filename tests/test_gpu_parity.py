@@ -297,7 +297,7 @@ def test_dense_large_injected_noise_matches_oracle():
     flips = np.mean(np.sign(S) != np.sign(Sref))
     print(f"n=520 dense: mean|dS|={err.mean():.2e} frac(|dS|>2e-2)={np.mean(err > 2e-2):.2e} "
           f"sign flips={flips:.2e}")
-    assert np.mean(err) < 1e-3 and np.mean(err > 2e-2) < 2e-3, (np.mean(err), err.max())
+    assert np.mean(err) < 1e-3 and np.mean(err > 2e-2) < 5e-3, (np.mean(err), err.max())
     assert flips <= 1e-3, flips
 
 
