@@ -31,7 +31,9 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-o", OUT + ".tmp", *sources()]
+    extra = os.environ.get("NMFA_NVCC_DEFS", "").split()   # experiment builds only
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", OUT + ".tmp",
+           *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -6,9 +6,11 @@
 // GEMM orientation: D[r, i] = sum_k S[r, k] J[i, k]
 //   M = replicas (256 per CTA pair, 128 per CTA), N = spins (tile of <= 256),
 //   K = spins.  A = S (fp16, K-major), B = J (fp16, K-major; J symmetric).
-// Operand images in HBM are pre-tiled so a (128 rows x 64 k) tile is 16 KB of
+// Operand images in HBM are pre-tiled so a (128 rows x 128 k) tile is 32 KB of
 // contiguous bytes in the UMMA canonical no-swizzle K-major layout:
-//   byte(row, k) = (k/64)*Rows*128 + (row/8)*1024 + ((k%64)/8)*128 + (row%8)*16 + (k%8)*2
+//   byte(row, k) = (k/128)*Rows*256 + (row/8)*2048 + ((k%128)/8)*128 + (row%8)*16 + (k%8)*2
+// (measured: the per-SM TMA engine costs ~100 cycles per box + ~11 cycles/KB,
+// so operands move in one 32 KB box each per stage; see profiles/).
 // TMA moves them as a 2-D tensor of 128-byte lines.  The epilogue writes the
 // next step's A image directly in that layout (two 16-B stores per 16
 // spins, a warp covers four full 128-B lines), so no transpose pass exists.
@@ -23,17 +25,22 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 #include "internal.h"
 
 namespace nmfa {
 
-constexpr int kDStages = 6;
+#ifndef NMFA_DSTAGES
+#define NMFA_DSTAGES 3
+#endif
+constexpr int kDStages = NMFA_DSTAGES;
+constexpr int kBK = 128;  // K per pipeline stage: one 32 KB TMA box per operand
 constexpr int kDEpiWarps = 16;
 constexpr int kDThreads = 128 + 32 * kDEpiWarps;
-constexpr uint32_t kATile = 128 * 128;
-constexpr uint32_t kBTileMax = 128 * 128;
+constexpr uint32_t kATile = 128 * kBK * 2;     // 128 rows x 128 k fp16 = 32 KB
+constexpr uint32_t kBTileMax = 128 * kBK * 2;  // <= 128 rows (N/2) x 128 k
 constexpr uint32_t kDStageBytes = kATile + kBTileMax;
 constexpr uint32_t kAccCols = 256;
 constexpr size_t kDSmemBytes = (size_t)kDStages * kDStageBytes + 1024;
@@ -50,7 +57,7 @@ struct DenseState {
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
   CUtensorMap tmA[2];
-  CUtensorMap tmB[5];  // box rows 8, 16, 32, 64, 128
+  CUtensorMap tmB[5];  // box lines 16, 32, 64, 128, 256 (= 8..128 rows)
 };
 
 struct DenseStepArgs {
@@ -71,6 +78,7 @@ struct DenseStepArgs {
   float* s_out;
   float* s_hist;
   int last;
+  unsigned long long* trace;  // debug: per-k-block timestamps (NMFA_DBG_TRACE)
 };
 
 // ---------------------------------------------------------------------------
@@ -133,11 +141,11 @@ __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
 template <bool kInjected>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_step_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB8,
                       const __grid_constant__ CUtensorMap tmB16,
                       const __grid_constant__ CUtensorMap tmB32,
                       const __grid_constant__ CUtensorMap tmB64,
-                      const __grid_constant__ CUtensorMap tmB128, const DenseStepArgs a) {
+                      const __grid_constant__ CUtensorMap tmB128,
+                      const __grid_constant__ CUtensorMap tmB256, const DenseStepArgs a) {
   extern __shared__ __align__(1024) uint8_t dsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -151,6 +159,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   const int j0 = a.tile_off[pair], j1 = a.tile_off[pair + 1];
 
   if (warp == 0 && lane == 0) {
+    const CUtensorMap* maps[6] = {&tmA, &tmB16, &tmB32, &tmB64, &tmB128, &tmB256};
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps[m])) : "memory");
     for (int s = 0; s < kDStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -179,18 +191,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
           const int s = it % kDStages;
           mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+#ifdef NMFA_DBG_TRACE
+          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 0) * 256 + it] = clock64();
+#endif
           const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
-          if (cta == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * 128u));
+          if (cta == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
           uint8_t* st = smem + (size_t)s * kDStageBytes;
-          tma2d_pair(smem_u32(st), &tmA, 0, (int)(kb * a.Rp) + arow, fb);
-          int off = 0;
+          tma2d_pair(smem_u32(st), &tmA, 0, (int)(kb * a.Rp + arow) * 2, fb);
+          int off = 0;  // rows
 #pragma unroll
           for (int b = 4; b >= 0; --b) {
             const int rows = 8 << b;
             if (half & rows) {
-              const CUtensorMap* tm = b == 4 ? &tmB128 : b == 3 ? &tmB64 : b == 2 ? &tmB32
-                                    : b == 1 ? &tmB16 : &tmB8;
-              tma2d_pair(smem_u32(st + kATile + off * 128), tm, 0, kb * a.np + brow + off, fb);
+              const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
+                                    : b == 1 ? &tmB32 : &tmB16;
+              tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
+                         (kb * a.np + brow + off) * 2, fb);
               off += rows;
             }
           }
@@ -205,19 +221,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const DenseTile tl = a.tiles[j];
         const int slot = jj & 1, use = jj >> 1;
         mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
+#ifdef NMFA_DBG_TRACE
+        if (a.trace && blockIdx.x < 2 && jj < 256) a.trace[(blockIdx.x * 4 + 3) * 256 + jj] = clock64();
+#endif
         tc_fence_after();
         const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
         const uint32_t d = tbase + (uint32_t)slot * kAccCols;
         for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
           const int s = it % kDStages;
+#ifdef NMFA_DBG_TRACE
+          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 1) * 256 + it] = clock64();
+#endif
           mbar_wait(&full_bar[s], (it / kDStages) & 1);
+#ifdef NMFA_DBG_TRACE
+          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 2) * 256 + it] = clock64();
+#endif
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + (size_t)s * kDStageBytes);
           const uint32_t sb = sa + kATile;
-          const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : 4;
+          const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : kBK / 16;
           for (int ks = 0; ks < nsub; ++ks) {
-            mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 1024),
-                     make_desc_noswizzle(sb + ks * 256, 128, 1024), idesc, (kb | ks) ? 1u : 0u);
+            mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 2048),
+                     make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (kb | ks) ? 1u : 0u);
           }
           commit_pair_mc(&empty_bar[s]);
         }
@@ -239,6 +264,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const unsigned long long key = a.key_base + (unsigned long long)r;
       const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
       mbar_wait(&tfull_bar[slot], use & 1);
+#ifdef NMFA_DBG_TRACE
+      int tq = 0;
+      if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4)
+        a.trace[8 * 256 + (e * 4 + jj) * 8 + tq++] = clock64();
+#endif
       tc_fence_after();
       const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
       const int nch = tl.nlen >> 4;
@@ -249,29 +279,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const int i0 = tl.n0 + 16 * c;
         float acc[16], ms[16];
         tmem_ld16(tacc + 16 * c, acc);
+#ifdef NMFA_DBG_NOEPI
+        tmem_wait_ld();
+        if (acc[0] == 12345.f) a.master[0] = acc[1];
+        continue;
+#endif
         float4* mrow = master4 + (long long)(i0 >> 2) * a.Rp + r;
+#ifndef NMFA_DBG_NOMASTER
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float4 m = mrow[q * a.Rp];
           ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
         }
+#else
+#pragma unroll
+        for (int q = 0; q < 16; ++q) ms[q] = 0.f;
+#endif
         tmem_wait_ld();
         const int nvalid = valid ? min(16, a.n - i0) : 0;
         const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + a.t) * a.n + i0 : nullptr;
+#ifndef NMFA_DBG_NOMATH
         update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
                             (uint32_t)(i0 / 4), (uint32_t)a.t, a.sigma, a.inv_t, a.alpha, a.oma);
+#else
+#pragma unroll
+        for (int q = 0; q < 16; ++q) ms[q] += acc[q];
+#endif
+#ifndef NMFA_DBG_NOMASTER
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           mrow[q * a.Rp] = make_float4(ms[4 * q], ms[4 * q + 1], ms[4 * q + 2], ms[4 * q + 3]);
+#endif
+#ifndef NMFA_DBG_NOIMG
         // next step's A operand image (pre-tiled K-major, see header)
-        uint8_t* img = a.a_next + (long long)(i0 >> 6) * a.Rp * 128 + (r >> 3) * 1024 +
-                       ((i0 & 63) >> 3) * 128 + (r & 7) * 16;
+        uint8_t* img = a.a_next + (long long)(i0 >> 7) * a.Rp * 256 + (r >> 3) * 2048 +
+                       ((i0 & 127) >> 3) * 128 + (r & 7) * 16;
         *reinterpret_cast<uint4*>(img) =
             make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
                        pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
         *reinterpret_cast<uint4*>(img + 128) =
             make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
                        pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
+#else
+        if (ms[3] == 1234.5f) a.master[1] = ms[7];
+#endif
+#ifdef NMFA_DBG_TRACE
+        if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4 && tq < 7)
+          a.trace[8 * 256 + (e * 4 + jj) * 8 + tq++] = clock64();
+#endif
         if (extra) {
           if (a.s_hist) {
             float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n + i0;
@@ -292,6 +347,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+#ifdef NMFA_DBG_TRACE
+      if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4)
+        a.trace[8 * 256 + (e * 4 + jj) * 8 + 7] = clock64();
+#endif
       if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
     }
   }
@@ -312,7 +371,7 @@ __global__ void dense_init_kernel(float* master, uint8_t* a_img, const float* s0
   const int i = (int)(e / Rp);
   const float v = (s0 && r < R && i < n) ? s0[r * n + i] : 0.f;
   if (i < np) master[((long long)(i >> 2) * Rp + r) * 4 + (i & 3)] = v;
-  const long long off = (long long)(i >> 6) * Rp * 128 + (r >> 3) * 1024 + ((i & 63) >> 3) * 128 +
+  const long long off = (long long)(i >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
                         (r & 7) * 16 + (i & 7) * 2;
   *reinterpret_cast<__half*>(a_img + off) = __float2half_rn(v);
 }
@@ -354,13 +413,13 @@ static int make_line_map(CUtensorMap* tm, void* base, uint64_t lines, uint32_t b
 }
 
 static inline size_t img_off(uint32_t row, uint32_t k, uint32_t rows) {
-  return (size_t)(k >> 6) * rows * 128 + (row >> 3) * 1024 + ((k & 63) >> 3) * 128 + (row & 7) * 16 +
-         (k & 7) * 2;
+  return (size_t)(k >> 7) * rows * 256 + (row >> 3) * 2048 + ((k & 127) >> 3) * 128 +
+         (row & 7) * 16 + (k & 7) * 2;
 }
 
 int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jd) {
   const uint32_t n = (uint32_t)p->n;
-  const uint32_t np = (n + 15) / 16 * 16, kp = (n + 63) / 64 * 64;
+  const uint32_t np = (n + 15) / 16 * 16, kp = (n + kBK - 1) / kBK * kBK;
   std::vector<__half> img((size_t)kp * np, __float2half(0.f));
   for (uint32_t i = 0; i < n; ++i)
     for (uint32_t k = 0; k < n; ++k) {
@@ -391,9 +450,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   pl->dense = ds;
   const int n = (int)p->n;
   ds->np = (n + 15) / 16 * 16;
-  ds->kp = (n + 63) / 64 * 64;
-  ds->kblocks = ds->kp / 64;
-  ds->k_last_sub = (n - (ds->kblocks - 1) * 64 + 15) / 16;
+  ds->kp = (n + kBK - 1) / kBK * kBK;
+  ds->kblocks = ds->kp / kBK;
+  ds->k_last_sub = (n - (ds->kblocks - 1) * kBK + 15) / 16;
   ds->Rp = (pl->R + 255) / 256 * 256;
   const size_t master_bytes = (size_t)(ds->np / 4) * ds->Rp * 16;
   const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
@@ -417,10 +476,10 @@ int dense_plan_alloc(nmfa_plan* pl) {
     while (u < u1) {
       const long long m = u / upm;
       const long long seg_end = std::min(u1, (m + 1) * upm);
-      const long long L = seg_end - u, nt = (L + 15) / 16;
-      for (long long k = 0; k < nt; ++k) {
-        const long long a0 = L * k / nt, a1 = L * (k + 1) / nt;
-        tiles.push_back({(int)m, (int)((u - m * upm + a0) * 16), (int)((a1 - a0) * 16), 0});
+      // full 256-spin tiles (one 32 KB B box per CTA and stage) + one remainder tile
+      for (long long a0 = u; a0 < seg_end; a0 += 16) {
+        const long long a1 = std::min(seg_end, a0 + 16);
+        tiles.push_back({(int)m, (int)((a0 - m * upm) * 16), (int)((a1 - a0) * 16), 0});
       }
       u = seg_end;
     }
@@ -435,10 +494,10 @@ int dense_plan_alloc(nmfa_plan* pl) {
 
   int err;
   for (int b = 0; b < 2; ++b)
-    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp, 128)))
+    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
       return err;
   for (int b = 0; b < 5; ++b)
-    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np, 8u << b)))
+    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np * 2, 16u << b)))
       return err;
   NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
@@ -481,6 +540,11 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
+#ifdef NMFA_DBG_TRACE
+  static unsigned long long* trace = nullptr;
+  if (!trace) cudaMallocManaged(&trace, 16 * 256 * 8);
+  a.trace = trace;
+#endif
   for (int t = 0; t < pl->t_f; ++t) {
     a.t = t;
     a.inv_t = pl->h_inv_temp[t];
@@ -491,6 +555,26 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
         ds->tmA[t & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
     NMFA_LAUNCH_CHECK();
   }
+#ifdef NMFA_DBG_TRACE
+  cudaStreamSynchronize(st);
+  {
+    FILE* f = fopen("gpurun_out/dense_trace.txt", "w");
+    for (int b = 0; b < 2; ++b)
+      for (int it = 0; it < 256; ++it)
+        fprintf(f, "%d %d %llu %llu %llu %llu\n", b, it, trace[(b * 4 + 0) * 256 + it],
+                trace[(b * 4 + 1) * 256 + it], trace[(b * 4 + 2) * 256 + it],
+                trace[(b * 4 + 3) * 256 + it]);
+    fclose(f);
+    f = fopen("gpurun_out/dense_trace_epi.txt", "w");
+    for (int e = 0; e < 16; ++e)
+      for (int jj = 0; jj < 4; ++jj) {
+        fprintf(f, "%d %d", e, jj);
+        for (int k = 0; k < 8; ++k) fprintf(f, " %llu", trace[8 * 256 + (e * 4 + jj) * 8 + k]);
+        fprintf(f, "\n");
+      }
+    fclose(f);
+  }
+#endif
   add_launches(1 + pl->t_f);
   return NMFA_OK;
 }
