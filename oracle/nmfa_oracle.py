@@ -153,19 +153,68 @@ def anneal(p, s, temps, noise, alpha, record=False):
     return s, s_hist, e_hist
 
 
-def run(p, seed, t_f=1000, alpha=0.15, sigma=0.15, temps=None):
+# Compiled restatement of the same loop for the CPU-baseline timing: the
+# reference's default backend is numba (kernels.py:16-27), so the port times
+# a jitted loop too.  dgemv via np.dot and libm tanh, as _kernels_numba.py:71-75
+# and 48-56 do; results agree with `anneal` to ~1e-12 (tests/test_oracle.py).
+try:
+    from numba import njit
+
+    @njit(nogil=True, cache=False)
+    def _loop_dense(J, h, norm, s, temps, noise, alpha):
+        for t in range(temps.shape[0]):
+            phi = (h + np.dot(J, s)) / norm + noise[t]
+            s = alpha * (-np.tanh(phi / temps[t])) + (1.0 - alpha) * s
+        return s
+
+    @njit(nogil=True, cache=False)
+    def _loop_sparse(indptr, indices, weights, h, norm, s, temps, noise, alpha):
+        n = s.shape[0]
+        phi = np.empty(n)
+        for t in range(temps.shape[0]):
+            for i in range(n):
+                acc = 0.0
+                for k in range(indptr[i], indptr[i + 1]):
+                    acc += weights[k] * s[indices[k]]
+                phi[i] = (h[i] + acc) / norm[i] + noise[t, i]
+            for i in range(n):
+                s[i] = alpha * (-np.tanh(phi[i] / temps[t])) + (1.0 - alpha) * s[i]
+        return s
+
+    HAVE_JIT = True
+except ImportError:  # pragma: no cover
+    HAVE_JIT = False
+
+
+def anneal_fast(p, s, temps, noise, alpha):
+    """Final state of `anneal` through the jitted loop (falls back to numpy)."""
+    if not HAVE_JIT:
+        return anneal(p, s, temps, noise, alpha)[0]
+    s = np.array(s, dtype=np.float64)
+    temps = np.asarray(temps, dtype=np.float64)
+    if p.is_dense:
+        return _loop_dense(p.dense, p.h, p.normalizers_safe, s, temps, noise, float(alpha))
+    return _loop_sparse(p.csr_indptr, p.csr_indices, p.csr_weights, p.h, p.normalizers_safe, s,
+                        temps, noise, float(alpha))
+
+
+def run(p, seed, t_f=1000, alpha=0.15, sigma=0.15, temps=None, jit=True):
     """One seeded run (solver.py:236-253): returns (config, energy)."""
     temps = temperatures(t_f) if temps is None else temps
-    s, _, _ = anneal(p, np.zeros(p.n), temps, run_noise(seed, t_f, p.n, sigma), alpha)
+    noise = run_noise(seed, t_f, p.n, sigma)
+    if jit:
+        s = anneal_fast(p, np.zeros(p.n), temps, noise, alpha)
+    else:
+        s, _, _ = anneal(p, np.zeros(p.n), temps, noise, alpha)
     cfg = sign_round(s)
     return cfg, energy(p, cfg)
 
 
-def batch(p, seed, n_runs, t_f=1000, alpha=0.15, sigma=0.15, threads=1):
+def batch(p, seed, n_runs, t_f=1000, alpha=0.15, sigma=0.15, threads=1, jit=True):
     """n_runs independent runs, run k seeded seed+k (solver.py:262-280)."""
     temps = temperatures(t_f)
     seeds = [(int(seed) + k) & MASK64 for k in range(int(n_runs))]
-    one = lambda sd: run(p, sd, t_f, alpha, sigma, temps)
+    one = lambda sd: run(p, sd, t_f, alpha, sigma, temps, jit)
     if threads <= 1:
         out = [one(sd) for sd in seeds]
     else:

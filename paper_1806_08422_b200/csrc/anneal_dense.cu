@@ -78,6 +78,9 @@ struct DenseStepArgs {
   float* s_out;
   float* s_hist;
   int last;
+  double* energy;        // energy mode: E[r] accumulator (zeroed)
+  const double* h;       // raw fields (energy mode)
+  double half_scale;     // 0.5 * j_scale (energy mode)
   unsigned long long* trace;  // debug: per-k-block timestamps (NMFA_DBG_TRACE)
 };
 
@@ -138,7 +141,9 @@ __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
       : "memory");
 }
 
-template <bool kInjected>
+// kEnergy: the A operand holds the +-1 configuration; the epilogue reduces
+// E_r = 1/2 c_r.(J c_r) + h.c_r exactly (integer J, |J c| < 2^24) instead of updating.
+template <bool kInjected, bool kEnergy>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_step_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB16,
@@ -275,6 +280,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const bool extra = valid && (a.s_hist != nullptr || a.last);
       const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
       const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+      if constexpr (kEnergy) {
+        double e_pair = 0.0, e_field = 0.0;
+        for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
+          const int i0 = tl.n0 + 16 * c;
+          float acc[16];
+          tmem_ld16(tacc + 16 * c, acc);
+          const float4* mrow = master4 + (long long)(i0 >> 2) * a.Rp + r;
+          float ms[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 m = mrow[q * a.Rp];
+            ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
+          }
+          tmem_wait_ld();
+          const int nvalid = valid ? min(16, a.n - i0) : 0;
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) {
+            if (cc < nvalid) {
+              const bool neg = ms[cc] < 0.f;                       // sign_round, problem.py:181
+              e_pair += (double)(neg ? -acc[cc] : acc[cc]);        // c_i (J c)_i, exact integers
+              const double hv = __ldg(a.h + i0 + cc);
+              e_field += neg ? -hv : hv;
+            }
+          }
+        }
+        if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
+      } else {
       for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
         const int i0 = tl.n0 + 16 * c;
         float acc[16], ms[16];
@@ -314,12 +346,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         // next step's A operand image (pre-tiled K-major, see header)
         uint8_t* img = a.a_next + (long long)(i0 >> 7) * a.Rp * 256 + (r >> 3) * 2048 +
                        ((i0 & 127) >> 3) * 128 + (r & 7) * 16;
-        *reinterpret_cast<uint4*>(img) =
-            make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
-                       pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
-        *reinterpret_cast<uint4*>(img + 128) =
-            make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
-                       pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
+        if (!a.last) {
+          *reinterpret_cast<uint4*>(img) =
+              make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
+                         pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
+          *reinterpret_cast<uint4*>(img + 128) =
+              make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
+                         pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
+        } else {  // the energy pass multiplies J by the rounded configuration
+          float sg[16];
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) sg[cc] = ms[cc] < 0.f ? -1.f : 1.f;
+          *reinterpret_cast<uint4*>(img) =
+              make_uint4(pack_half2(sg[0], sg[1]), pack_half2(sg[2], sg[3]),
+                         pack_half2(sg[4], sg[5]), pack_half2(sg[6], sg[7]));
+          *reinterpret_cast<uint4*>(img + 128) =
+              make_uint4(pack_half2(sg[8], sg[9]), pack_half2(sg[10], sg[11]),
+                         pack_half2(sg[12], sg[13]), pack_half2(sg[14], sg[15]));
+        }
 #else
         if (ms[3] == 1234.5f) a.master[1] = ms[7];
 #endif
@@ -344,6 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             }
           }
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -499,16 +544,18 @@ int dense_plan_alloc(nmfa_plan* pl) {
   for (int b = 0; b < 5; ++b)
     if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np * 2, 16u << b)))
       return err;
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false>,
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<true>,
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
   return NMFA_OK;
 }
 
 int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
-                        cudaStream_t st) {
+                        double* energy, bool* energy_done, cudaStream_t st) {
   const nmfa_problem* p = pl->p;
   auto* ds = static_cast<DenseState*>(pl->dense);
   if (!ds) {
@@ -550,7 +597,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
     a.inv_t = pl->h_inv_temp[t];
     a.last = (t == pl->t_f - 1);
     a.a_next = ds->a_img[(t + 1) & 1];
-    auto kern = noise ? dense_step_kernel<true> : dense_step_kernel<false>;
+    auto kern = noise ? dense_step_kernel<true, false> : dense_step_kernel<false, false>;
     kern<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
         ds->tmA[t & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
     NMFA_LAUNCH_CHECK();
@@ -576,7 +623,26 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   }
 #endif
   add_launches(1 + pl->t_f);
+  *energy_done = false;
+  if (energy && dense_energy_exact(p)) {
+    // one more GEMM pass over the +-1 configuration image (written by the last step)
+    NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
+    a.energy = energy;
+    a.h = p->d_h;
+    a.half_scale = 0.5 * p->j_scale;
+    a.last = 0;
+    a.t = pl->t_f;
+    dense_step_kernel<false, true><<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
+        ds->tmA[pl->t_f & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
+    NMFA_LAUNCH_CHECK();
+    add_launches(1);
+    *energy_done = true;
+  }
   return NMFA_OK;
+}
+
+bool dense_energy_exact(const nmfa_problem* p) {
+  return p->int_weights && p->j_exact && p->max_row_abs / p->j_scale < 16777216.0;
 }
 
 }  // namespace nmfa

@@ -46,6 +46,7 @@ int64_t nmfa_last_launch_count(void) { return g_launches; }
 
 int nmfa_problem_destroy(nmfa_problem_t* p) {
   if (!p) return NMFA_OK;
+  if (p->cached_plan) nmfa_plan_destroy(p->cached_plan);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
@@ -177,6 +178,14 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
     if (!exact1) scale = std::ldexp(1.0, (int)std::ceil(std::log2(wmax)));  // |J/scale| <= 1
   }
   p->j_scale = scale;
+  {
+    std::vector<double> rs(n, 0.0);
+    for (int64_t k = 0; k < n_edges; ++k) {
+      rs[lo[k]] += std::fabs(w[k]);
+      rs[hi[k]] += std::fabs(w[k]);
+    }
+    for (int64_t i = 0; i < n; ++i) p->max_row_abs = std::max(p->max_row_abs, rs[i]);
+  }
   bool jex = true;
   for (int64_t k = 0; k < n_edges && jex; ++k) jex = exact_in_half(w[k] / scale);
   p->j_exact = jex;
@@ -388,17 +397,19 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
   cudaSetDevice(p->device);
   uint64_t key_base = seed + (uint64_t)r0;
   int err = NMFA_OK;
+  bool energy_done = false;
   switch (p->path) {
     case NMFA_PATH_SMALL:
       err = launch_small_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
       break;
     case NMFA_PATH_DENSE:
-      err = launch_dense_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
+      err = launch_dense_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, energy, &energy_done,
+                                st);
       break;
     default:
       err = launch_sparse_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
   }
-  if (!err && energy)
+  if (!err && energy && !energy_done)
     err = launch_energy(p, cfg, pl->R, energy, pl->d_bits, pl->d_epart, pl->energy_chunks, st);
   if (!err && e_hist) {
     // energies of sign(s_t) for every recorded step (_kernels_numba.py:57-60)
@@ -424,21 +435,33 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
   return err;
 }
 
-int nmfa_anneal(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
+int nmfa_anneal(const nmfa_problem_t* cp, int64_t R, int32_t t_f, const double* temps,
                 double alpha, double sigma, uint64_t seed, int64_t r0, const float* noise,
                 const float* s0, int8_t* cfg, double* energy, float* s_out, float* s_hist,
                 double* e_hist, void* stream) {
-  nmfa_plan_t* pl = nullptr;
-  int err = nmfa_plan_create(p, R, t_f, temps, alpha, sigma, &pl);
-  if (err) return err;
-  err = nmfa_plan_run(pl, seed, r0, noise, s0, cfg, energy, s_out, s_hist, e_hist, stream);
-  int64_t launches = g_launches;
+  if (!cp) return arg_error("NULL problem");
+  if (!temps || t_f < 1) return arg_error("t_f must be at least 1, got " + std::to_string(t_f));
+  auto* p = const_cast<nmfa_problem*>(cp);  // only the plan cache is mutated
+  std::lock_guard<std::mutex> lock(p->cache_mu);
+  nmfa_plan_t* pl = p->cached_plan;
+  const bool hit = pl && pl->R == R && pl->t_f == t_f && p->cached_alpha == alpha &&
+                   p->cached_sigma == sigma &&
+                   std::equal(temps, temps + t_f, p->cached_temps.begin(), p->cached_temps.end());
+  if (!hit) {
+    if (pl) nmfa_plan_destroy(pl);
+    p->cached_plan = nullptr;
+    int err = nmfa_plan_create(p, R, t_f, temps, alpha, sigma, &pl);
+    if (err) return err;
+    p->cached_plan = pl;
+    p->cached_temps.assign(temps, temps + t_f);
+    p->cached_alpha = alpha;
+    p->cached_sigma = sigma;
+  }
+  int err = nmfa_plan_run(pl, seed, r0, noise, s0, cfg, energy, s_out, s_hist, e_hist, stream);
   if (!err && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
     set_error(std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
     err = NMFA_ERR_CUDA;
   }
-  nmfa_plan_destroy(pl);
-  g_launches = launches;
   return err;
 }
 
@@ -446,28 +469,36 @@ int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
                      double alpha, double sigma, uint64_t seed, int64_t r0, int8_t* cfg_host,
                      double* energy_host) {
   if (!p || !cfg_host) return arg_error("NULL argument");
+  if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   int8_t* d_cfg = nullptr;
   double* d_e = nullptr;
+  cudaStream_t st = nullptr;
   int err = NMFA_OK;
-  if (cudaMalloc(&d_cfg, (size_t)R * p->n) != cudaSuccess ||
-      cudaMalloc(&d_e, (size_t)R * 8) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocAsync(&d_cfg, (size_t)R * p->n, st) != cudaSuccess ||
+      cudaMallocAsync(&d_e, (size_t)R * 8, st) != cudaSuccess) {
     set_error("out of device memory");
     err = NMFA_ERR_CUDA;
   }
   if (!err)
     err = nmfa_anneal(p, R, t_f, temps, alpha, sigma, seed, r0, nullptr, nullptr, d_cfg,
-                      energy_host ? d_e : nullptr, nullptr, nullptr, nullptr, nullptr);
-  if (!err && (cudaMemcpy(cfg_host, d_cfg, (size_t)R * p->n, cudaMemcpyDeviceToHost) ||
-               (energy_host &&
-                cudaMemcpy(energy_host, d_e, (size_t)R * 8, cudaMemcpyDeviceToHost)))) {
+                      energy_host ? d_e : nullptr, nullptr, nullptr, nullptr, st);
+  if (!err && (cudaMemcpyAsync(cfg_host, d_cfg, (size_t)R * p->n, cudaMemcpyDeviceToHost, st) ||
+               (energy_host && cudaMemcpyAsync(energy_host, d_e, (size_t)R * 8,
+                                               cudaMemcpyDeviceToHost, st)) ||
+               cudaStreamSynchronize(st))) {
     set_error("device to host copy failed");
     err = NMFA_ERR_CUDA;
   }
-  if (d_cfg) cudaFree(d_cfg);
-  if (d_e) cudaFree(d_e);
+  if (d_cfg) cudaFreeAsync(d_cfg, st);
+  if (d_e) cudaFreeAsync(d_e, st);
+  if (st) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
   cudaSetDevice(prev);
   return err;
 }

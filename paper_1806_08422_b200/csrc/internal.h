@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,6 +41,7 @@ struct nmfa_problem {
   bool j_exact = true;
   bool int_weights = true;
   double j_scale = 1.0;    // J_dev = J / j_scale (power of two); inv_norm carries j_scale
+  double max_row_abs = 0.0; // max_i sum_j |J_ij| (exactness bound of tensor-core energies)
   int32_t np = 0;          // n padded to a multiple of 16 (tensor-core paths)
 
   std::vector<double> h, norm_safe;  // host copies (float64)
@@ -61,6 +63,12 @@ struct nmfa_problem {
   int32_t* d_e_j = nullptr;
   double* d_e_w = nullptr;
   double* d_h = nullptr;
+  // one-shot entry points (nmfa_anneal / nmfa_anneal_host) reuse one cached
+  // plan; the mutex serialises them (they are synchronous).
+  std::mutex cache_mu;
+  nmfa_plan* cached_plan = nullptr;
+  std::vector<double> cached_temps;
+  double cached_alpha = -1.0, cached_sigma = -1.0;
 };
 
 struct nmfa_plan {
@@ -94,7 +102,8 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
                          cudaStream_t st);
 int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
-                        cudaStream_t st);
+                        double* energy, bool* energy_done, cudaStream_t st);
+bool dense_energy_exact(const nmfa_problem* p);
 int dense_plan_alloc(nmfa_plan* pl);
 void dense_plan_free(nmfa_plan* pl);
 int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jdense_rowmajor);

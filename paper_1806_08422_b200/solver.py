@@ -271,7 +271,8 @@ def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=Non
         s0 = torch.as_tensor(s0, dtype=torch.float32, device=dev).contiguous()
         if tuple(s0.shape) != (n_runs, n):
             raise ValueError(f"s0 length does not match problem size {n}")
-    plan = Plan(problem, n_runs, temps, params.alpha, params.sigma, device)
+    temps = np.ascontiguousarray(temps, dtype=np.float64)
+    handle = problem.device_handle(device).handle
     cfg = torch.empty((n_runs, n), dtype=torch.int8, device=dev)
     en = torch.empty(n_runs, dtype=torch.float64, device=dev)
     s_final = torch.empty((n_runs, n), dtype=torch.float32, device=dev) if return_s else None
@@ -279,10 +280,15 @@ def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=Non
     if record_trajectory:
         s_hist = torch.empty((n_runs, t_f, n), dtype=torch.float32, device=dev)
         e_hist = torch.empty((n_runs, t_f), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    plan.run(params.seed, r0, noise, s0, cfg, en, s_final, s_hist, e_hist)
-    torch.cuda.synchronize(dev)
+    # one-shot C-ABI entry: reuses the device plan cached on the problem handle
+    _native.check(_native.load().nmfa_anneal(
+        handle, n_runs, t_f, _native.ptr(temps), float(params.alpha), float(params.sigma),
+        int(params.seed) & MASK64, int(r0), _native.ptr(noise), _native.ptr(s0), _native.ptr(cfg),
+        _native.ptr(en), _native.ptr(s_final), _native.ptr(s_hist), _native.ptr(e_hist),
+        ctypes.c_void_p(stream.cuda_stream)))
     wall = time.perf_counter() - t0
     return SampleSet(cfg, en, int(params.seed), int(r0), wall, s_final, s_hist, e_hist)
 

@@ -104,13 +104,27 @@ def test_run_with_noise_sk100_long(G):
     assert np.array_equal(O.sign_round(s), O.sign_round(T["sk100_s0_s"]))
 
 
-def test_batch_matches_reference_seeded(G):
+@pytest.mark.parametrize("jit", [False, True])
+def test_batch_matches_reference_seeded(G, jit):
     B = G["batches"]
     I = G["instances"]
     p = O.problem_from_edges(16, I["moebius16_ei"], I["moebius16_ej"], I["moebius16_w"])
-    cfg, e = O.batch(p, 0, 100, t_f=100, threads=4)
+    cfg, e = O.batch(p, 0, 100, t_f=100, threads=4, jit=jit)
     assert np.array_equal(e, B["moebius16_tf100_E"])
     assert np.array_equal(cfg.astype(np.int8), B["moebius16_tf100_cfg"])
+    p = O.problem_from_edges(100, I["sk100_s0_ei"], I["sk100_s0_ej"], I["sk100_s0_w"])
+    cfg, e = O.batch(p, 0, 8, t_f=1000, threads=4, jit=jit)
+    assert np.array_equal(e, B["sk100_tf1000_E"][:8])
+
+
+def test_jit_loop_matches_numpy_loop(G):
+    I = G["instances"]
+    for name, n in (("cubic40_s1", 40), ("sk30_s2", 30)):
+        p = O.problem_from_edges(n, I[name + "_ei"], I[name + "_ej"], I[name + "_w"])
+        noise = O.run_noise(4, 200, n, 0.15)
+        a = O.anneal(p, np.zeros(n), O.temperatures(200), noise, 0.15)[0]
+        b = O.anneal_fast(p, np.zeros(n), O.temperatures(200), noise, 0.15)
+        assert np.allclose(a, b, rtol=0, atol=1e-10)
 
 
 def test_batched_restatement_equals_reference_energies(G):
