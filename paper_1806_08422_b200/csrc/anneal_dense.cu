@@ -52,7 +52,7 @@ struct DenseTile {
 struct DenseState {
   int np = 0, kp = 0, kblocks = 0, k_last_sub = 0, pairs = 0;
   long long Rp = 0;
-  float* master = nullptr;
+  uint8_t* lo_img = nullptr;
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
@@ -70,8 +70,9 @@ struct DenseStepArgs {
   float inv_t, alpha, oma, sigma;
   const float* invn;
   const float* hn;
-  float* master;
+  const uint8_t* a_cur;  // this step's operand image (hi part of the state)
   uint8_t* a_next;
+  uint8_t* lo;           // residual image, same layout
   unsigned long long key_base;
   const float* noise;
   int8_t* cfg;
@@ -256,11 +257,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------- fused NMFA epilogue -------------------------
+    // State per (replica r, spin i): hi = fp16(s) lives in the operand image
+    // the TMA is reading this step (a_cur), lo = fp16(s - hi) in a second image
+    // of the same layout, so s = hi + lo carries ~22 bits and the whole
+    // per-step working set (2 images + lo + J) stays L2-resident.
     const int e = warp - 4, quarter = e & 3, hpart = e >> 2;  // 4 lane quarters x 4 column parts
     const int row = 32 * quarter + lane;
     const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
     const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
-    float4* master4 = reinterpret_cast<float4*>(a.master);
+    const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
+    const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
     for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
       const DenseTile tl = a.tiles[j];
       const int slot = jj & 1, use = jj >> 1;
@@ -268,134 +274,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const bool valid = r < a.R;
       const unsigned long long key = a.key_base + (unsigned long long)r;
       const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
+      const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
       mbar_wait(&tfull_bar[slot], use & 1);
-#ifdef NMFA_DBG_TRACE
-      int tq = 0;
-      if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4)
-        a.trace[8 * 256 + (e * 4 + jj) * 8 + tq++] = clock64();
-#endif
       tc_fence_after();
       const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
       const int nch = tl.nlen >> 4;
-      const bool extra = valid && (a.s_hist != nullptr || a.last);
-      const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
-      const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
       if constexpr (kEnergy) {
+        // a_cur holds the +-1 configuration written by the last anneal step
         double e_pair = 0.0, e_field = 0.0;
         for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
           const int i0 = tl.n0 + 16 * c;
           float acc[16];
           tmem_ld16(tacc + 16 * c, acc);
-          const float4* mrow = master4 + (long long)(i0 >> 2) * a.Rp + r;
-          float ms[16];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 m = mrow[q * a.Rp];
-            ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
-          }
+          const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
+          const uint4 c0 = *reinterpret_cast<const uint4*>(a.a_cur + off);
+          const uint4 c1 = *reinterpret_cast<const uint4*>(a.a_cur + off + 128);
+          float cs[16];
+          unpack_half8(c0, cs);
+          unpack_half8(c1, cs + 8);
           tmem_wait_ld();
           const int nvalid = valid ? min(16, a.n - i0) : 0;
 #pragma unroll
           for (int cc = 0; cc < 16; ++cc) {
             if (cc < nvalid) {
-              const bool neg = ms[cc] < 0.f;                       // sign_round, problem.py:181
-              e_pair += (double)(neg ? -acc[cc] : acc[cc]);        // c_i (J c)_i, exact integers
+              e_pair += (double)(cs[cc] * acc[cc]);                // c_i (J c)_i, exact integers
               const double hv = __ldg(a.h + i0 + cc);
-              e_field += neg ? -hv : hv;
+              e_field += cs[cc] < 0.f ? -hv : hv;
             }
           }
         }
         if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
       } else {
-      for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
-        const int i0 = tl.n0 + 16 * c;
-        float acc[16], ms[16];
-        tmem_ld16(tacc + 16 * c, acc);
-#ifdef NMFA_DBG_NOEPI
-        tmem_wait_ld();
-        if (acc[0] == 12345.f) a.master[0] = acc[1];
-        continue;
-#endif
-        float4* mrow = master4 + (long long)(i0 >> 2) * a.Rp + r;
-#ifndef NMFA_DBG_NOMASTER
+        const bool extra = valid && (a.s_hist != nullptr || a.last);
+        for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
+          const int i0 = tl.n0 + 16 * c;
+          float acc[16], ms[16], lo[16];
+          tmem_ld16(tacc + 16 * c, acc);
+          const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
+          const uint4 h0 = *reinterpret_cast<const uint4*>(a.a_cur + off);
+          const uint4 h1 = *reinterpret_cast<const uint4*>(a.a_cur + off + 128);
+          const uint4 l0 = *reinterpret_cast<const uint4*>(a.lo + off);
+          const uint4 l1 = *reinterpret_cast<const uint4*>(a.lo + off + 128);
+          unpack_half8(h0, ms);
+          unpack_half8(h1, ms + 8);
+          unpack_half8(l0, lo);
+          unpack_half8(l1, lo + 8);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 m = mrow[q * a.Rp];
-          ms[4 * q] = m.x; ms[4 * q + 1] = m.y; ms[4 * q + 2] = m.z; ms[4 * q + 3] = m.w;
-        }
-#else
+          for (int cc = 0; cc < 16; ++cc) ms[cc] += lo[cc];
+          tmem_wait_ld();
+          const int nvalid = valid ? min(16, a.n - i0) : 0;
+          const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + a.t) * a.n + i0 : nullptr;
+          update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
+                              (uint32_t)(i0 / 4), (uint32_t)a.t, a.sigma, a.inv_t, a.alpha, a.oma);
+          // split s -> (hi, lo); the last step writes the +-1 configuration for the energy pass
+          uint4 hv[2], lv[2];
+          split_half16(ms, hv, lv, a.last != 0);
+          *reinterpret_cast<uint4*>(a.a_next + off) = hv[0];
+          *reinterpret_cast<uint4*>(a.a_next + off + 128) = hv[1];
+          *reinterpret_cast<uint4*>(a.lo + off) = lv[0];
+          *reinterpret_cast<uint4*>(a.lo + off + 128) = lv[1];
+          if (extra) {
+            if (a.s_hist) {
+              float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n + i0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) ms[q] = 0.f;
-#endif
-        tmem_wait_ld();
-        const int nvalid = valid ? min(16, a.n - i0) : 0;
-        const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + a.t) * a.n + i0 : nullptr;
-#ifndef NMFA_DBG_NOMATH
-        update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
-                            (uint32_t)(i0 / 4), (uint32_t)a.t, a.sigma, a.inv_t, a.alpha, a.oma);
-#else
+              for (int cc = 0; cc < 16; ++cc)
+                if (cc < nvalid) hrow[cc] = ms[cc];
+            }
+            if (a.last) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) ms[q] += acc[q];
-#endif
-#ifndef NMFA_DBG_NOMASTER
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          mrow[q * a.Rp] = make_float4(ms[4 * q], ms[4 * q + 1], ms[4 * q + 2], ms[4 * q + 3]);
-#endif
-#ifndef NMFA_DBG_NOIMG
-        // next step's A operand image (pre-tiled K-major, see header)
-        uint8_t* img = a.a_next + (long long)(i0 >> 7) * a.Rp * 256 + (r >> 3) * 2048 +
-                       ((i0 & 127) >> 3) * 128 + (r & 7) * 16;
-        if (!a.last) {
-          *reinterpret_cast<uint4*>(img) =
-              make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
-                         pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
-          *reinterpret_cast<uint4*>(img + 128) =
-              make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
-                         pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
-        } else {  // the energy pass multiplies J by the rounded configuration
-          float sg[16];
-#pragma unroll
-          for (int cc = 0; cc < 16; ++cc) sg[cc] = ms[cc] < 0.f ? -1.f : 1.f;
-          *reinterpret_cast<uint4*>(img) =
-              make_uint4(pack_half2(sg[0], sg[1]), pack_half2(sg[2], sg[3]),
-                         pack_half2(sg[4], sg[5]), pack_half2(sg[6], sg[7]));
-          *reinterpret_cast<uint4*>(img + 128) =
-              make_uint4(pack_half2(sg[8], sg[9]), pack_half2(sg[10], sg[11]),
-                         pack_half2(sg[12], sg[13]), pack_half2(sg[14], sg[15]));
-        }
-#else
-        if (ms[3] == 1234.5f) a.master[1] = ms[7];
-#endif
-#ifdef NMFA_DBG_TRACE
-        if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4 && tq < 7)
-          a.trace[8 * 256 + (e * 4 + jj) * 8 + tq++] = clock64();
-#endif
-        if (extra) {
-          if (a.s_hist) {
-            float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n + i0;
-            #pragma unroll
-            for (int cc = 0; cc < 16; ++cc)
-              if (cc < nvalid) hrow[cc] = ms[cc];
-          }
-          if (a.last) {
-#pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
-              if (cc < nvalid) {
-                a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;
-                if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
+              for (int cc = 0; cc < 16; ++cc) {
+                if (cc < nvalid) {
+                  a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181
+                  if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
+                }
               }
             }
           }
         }
       }
-      }
       tc_fence_before();
       __syncwarp();
-#ifdef NMFA_DBG_TRACE
-      if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 4)
-        a.trace[8 * 256 + (e * 4 + jj) * 8 + 7] = clock64();
-#endif
       if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
     }
   }
@@ -407,18 +365,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   }
 }
 
-// master[i/4][r][i%4] and A image 0 from s0 (or zeros)
-__global__ void dense_init_kernel(float* master, uint8_t* a_img, const float* s0, int n, int np,
-                                  int kp, long long R, long long Rp) {
+// A image 0 (hi) and the lo image from s0 (or zeros); padding stays zero.
+__global__ void dense_init_kernel(uint8_t* a_img, uint8_t* lo_img, const float* s0, int n, int kp,
+                                  long long R, long long Rp) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)kp * Rp) return;
   const long long r = e % Rp;
   const int i = (int)(e / Rp);
   const float v = (s0 && r < R && i < n) ? s0[r * n + i] : 0.f;
-  if (i < np) master[((long long)(i >> 2) * Rp + r) * 4 + (i & 3)] = v;
   const long long off = (long long)(i >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
                         (r & 7) * 16 + (i & 7) * 2;
-  *reinterpret_cast<__half*>(a_img + off) = __float2half_rn(v);
+  const __half h = __float2half_rn(v);
+  *reinterpret_cast<__half*>(a_img + off) = h;
+  *reinterpret_cast<__half*>(lo_img + off) = __float2half_rn(v - __half2float(h));
 }
 
 // ---------------------------------------------------------------------------
@@ -480,7 +439,7 @@ int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jd) {
 void dense_plan_free(nmfa_plan* pl) {
   auto* ds = static_cast<DenseState*>(pl->dense);
   if (!ds) return;
-  if (ds->master) cudaFree(ds->master);
+  if (ds->lo_img) cudaFree(ds->lo_img);
   if (ds->a_img[0]) cudaFree(ds->a_img[0]);
   if (ds->a_img[1]) cudaFree(ds->a_img[1]);
   if (ds->d_tiles) cudaFree(ds->d_tiles);
@@ -499,9 +458,8 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->kblocks = ds->kp / kBK;
   ds->k_last_sub = (n - (ds->kblocks - 1) * kBK + 15) / 16;
   ds->Rp = (pl->R + 255) / 256 * 256;
-  const size_t master_bytes = (size_t)(ds->np / 4) * ds->Rp * 16;
   const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
-  NMFA_CUDA_TRY(cudaMalloc(&ds->master, master_bytes));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->lo_img, img_bytes));
   NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[0], img_bytes));
   NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[1], img_bytes));
   NMFA_CUDA_TRY(cudaMemset(ds->a_img[0], 0, img_bytes));
@@ -564,7 +522,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   }
   const long long tot = (long long)ds->kp * ds->Rp;
   dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-      ds->master, ds->a_img[0], s0, (int)p->n, ds->np, ds->kp, pl->R, ds->Rp);
+      ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
   NMFA_LAUNCH_CHECK();
   DenseStepArgs a{};
   a.tiles = ds->d_tiles;
@@ -581,7 +539,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.sigma = pl->sigma;
   a.invn = p->d_invn;
   a.hn = p->d_hn;
-  a.master = ds->master;
+  a.lo = ds->lo_img;
   a.key_base = key_base;
   a.noise = noise;
   a.cfg = cfg;
@@ -596,6 +554,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
     a.t = t;
     a.inv_t = pl->h_inv_temp[t];
     a.last = (t == pl->t_f - 1);
+    a.a_cur = ds->a_img[t & 1];
     a.a_next = ds->a_img[(t + 1) & 1];
     auto kern = noise ? dense_step_kernel<true, false> : dense_step_kernel<false, false>;
     kern<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
@@ -632,6 +591,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
     a.half_scale = 0.5 * p->j_scale;
     a.last = 0;
     a.t = pl->t_f;
+    a.a_cur = ds->a_img[pl->t_f & 1];
     dense_step_kernel<false, true><<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
         ds->tmA[pl->t_f & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
     NMFA_LAUNCH_CHECK();

@@ -300,6 +300,39 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void unpack_half8(const uint4 v, float f[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+
+// s -> hi = fp16(s), lo = fp16(s - hi)  (or hi = sign(s), lo = 0 when `sign`)
+__device__ __forceinline__ void split_half16(const float s[16], uint4 hi[2], uint4 lo[2],
+                                             bool sign) {
+  uint32_t h[8], l[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float a = s[2 * k], b = s[2 * k + 1];
+    if (sign) {
+      a = a < 0.f ? -1.f : 1.f;
+      b = b < 0.f ? -1.f : 1.f;
+    }
+    const __half2 hh = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[k] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi[0] = make_uint4(h[0], h[1], h[2], h[3]);
+  hi[1] = make_uint4(h[4], h[5], h[6], h[7]);
+  lo[0] = make_uint4(l[0], l[1], l[2], l[3]);
+  lo[1] = make_uint4(l[4], l[5], l[6], l[7]);
+}
+
 // Byte offset of element (row, k) inside a K-major no-swizzle UMMA operand
 // image whose rows are grouped 8 at a time (SBO = 128 B) and whose K core
 // matrices are `lbo` bytes apart.
