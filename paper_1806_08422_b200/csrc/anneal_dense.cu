@@ -15,9 +15,13 @@
 // next step's A image directly in that layout (two 16-B stores per 16
 // spins, a warp covers four full 128-B lines), so no transpose pass exists.
 //
-// Roles per CTA (640 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
-// CTA only), warp 2 TMEM allocator, warps 4-19 epilogue (lane quarter x column
-// quarter; 4 warps per scheduler to hide the Philox/MUFU latency chains).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
+// Roles per CTA (640 threads): warps 0-15 epilogue (lane quarter x column
+// quarter; 4 warps per scheduler to hide the Philox/MUFU latency chains),
+// warp 16 TMA producer, warp 17 MMA issuer (leader CTA only), warp 18 TMEM
+// allocator.  The control roles take the HIGHEST warp ids on purpose: the
+// warp scheduler favours high ids, and with low ids the producer and MMA
+// issuer starved behind the epilogue warps (measured: 3x longer k-block
+// intervals, see profiles/).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
 // accumulator slots of 256 columns so the epilogue of tile j overlaps the MMAs
 // of tile j+1.  Each pair owns a contiguous slice of the (replica block,
 // 16-spin unit) space, balanced to within one unit across the 74 pairs.
@@ -37,8 +41,12 @@ namespace nmfa {
 #endif
 constexpr int kDStages = NMFA_DSTAGES;
 constexpr int kBK = 128;  // K per pipeline stage: one 32 KB TMA box per operand
-constexpr int kDEpiWarps = 16;
-constexpr int kDThreads = 128 + 32 * kDEpiWarps;
+#ifndef NMFA_EPI_WARPS
+#define NMFA_EPI_WARPS 16
+#endif
+constexpr int kDEpiWarps = NMFA_EPI_WARPS;
+constexpr int kDThreads = 32 * kDEpiWarps + 128;
+constexpr int kWarpProducer = kDEpiWarps, kWarpMma = kDEpiWarps + 1, kWarpAlloc = kDEpiWarps + 2;
 constexpr uint32_t kATile = 128 * kBK * 2;     // 128 rows x 128 k fp16 = 32 KB
 constexpr uint32_t kBTileMax = 128 * kBK * 2;  // <= 128 rows (N/2) x 128 k
 constexpr uint32_t kDStageBytes = kATile + kBTileMax;
@@ -56,6 +64,9 @@ struct DenseState {
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
+  int* d_m_tiles = nullptr;       // tiles per replica block
+  unsigned* d_ready = nullptr;    // per replica block readiness counters
+  int n_mblk = 0;
   CUtensorMap tmA[2];
   CUtensorMap tmB[5];  // box lines 16, 32, 64, 128, 256 (= 8..128 rows)
 };
@@ -63,26 +74,28 @@ struct DenseState {
 struct DenseStepArgs {
   const DenseTile* tiles;
   const int* tile_off;
+  const int* m_tiles;      // tiles per replica block (whole schedule)
+  unsigned* ready;         // per replica block: (CTA, tile) epilogues completed this launch
   int kblocks, k_last_sub;
   int n, np;
   long long R, Rp;
-  int t, t_f;
-  float inv_t, alpha, oma, sigma;
+  int t_begin, t_end, t_f;  // sweeps [t_begin, t_end) of t_f; energy pass after t_f-1
+  int energy_pass;
+  float alpha, oma, sigma;
+  const float* inv_temp;
   const float* invn;
   const float* hn;
-  const uint8_t* a_cur;  // this step's operand image (hi part of the state)
-  uint8_t* a_next;
-  uint8_t* lo;           // residual image, same layout
+  uint8_t* img0;           // operand images (hi part of the state), ping-pong by parity
+  uint8_t* img1;
+  uint8_t* lo;             // residual image, same layout
   unsigned long long key_base;
   const float* noise;
   int8_t* cfg;
   float* s_out;
   float* s_hist;
-  int last;
-  double* energy;        // energy mode: E[r] accumulator (zeroed)
-  const double* h;       // raw fields (energy mode)
-  double half_scale;     // 0.5 * j_scale (energy mode)
-  unsigned long long* trace;  // debug: per-k-block timestamps (NMFA_DBG_TRACE)
+  double* energy;          // energy pass: E[r] accumulator (zeroed)
+  const double* h;         // raw fields (energy pass)
+  double half_scale;       // 0.5 * j_scale (energy pass)
 };
 
 // ---------------------------------------------------------------------------
@@ -142,16 +155,31 @@ __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
       : "memory");
 }
 
-// kEnergy: the A operand holds the +-1 configuration; the epilogue reduces
-// E_r = 1/2 c_r.(J c_r) + h.c_r exactly (integer J, |J c| < 2^24) instead of updating.
-template <bool kInjected, bool kEnergy>
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Persistent multi-sweep kernel.  Every pair walks its static tile list once
+// per sweep t in [t_begin, t_end) and then (energy_pass) once more in energy
+// mode: the A operand is then the +-1 configuration written by the last sweep
+// and the epilogue reduces E_r = 1/2 c_r.(J c_r) + h.c_r exactly (integer J,
+// |J c| < 2^24).  Sweep t+1 of replica block m may start once every (CTA, tile)
+// epilogue of block m for sweep t has published its rows (`ready[m]`), which is
+// the only inter-CTA dependency: replica blocks are independent.
+template <bool kInjected>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
-    dense_step_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB16,
-                      const __grid_constant__ CUtensorMap tmB32,
-                      const __grid_constant__ CUtensorMap tmB64,
-                      const __grid_constant__ CUtensorMap tmB128,
-                      const __grid_constant__ CUtensorMap tmB256, const DenseStepArgs a) {
+    dense_anneal_kernel(const __grid_constant__ CUtensorMap tmA0,
+                        const __grid_constant__ CUtensorMap tmA1,
+                        const __grid_constant__ CUtensorMap tmB16,
+                        const __grid_constant__ CUtensorMap tmB32,
+                        const __grid_constant__ CUtensorMap tmB64,
+                        const __grid_constant__ CUtensorMap tmB128,
+                        const __grid_constant__ CUtensorMap tmB256, const DenseStepArgs a) {
   extern __shared__ __align__(1024) uint8_t dsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -163,11 +191,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   const uint32_t cta = cluster_rank();
   const int pair = blockIdx.x >> 1;
   const int j0 = a.tile_off[pair], j1 = a.tile_off[pair + 1];
+  const int n_phases = (a.t_end - a.t_begin) + (a.energy_pass ? 1 : 0);
 
-  if (warp == 0 && lane == 0) {
-    const CUtensorMap* maps[6] = {&tmA, &tmB16, &tmB32, &tmB64, &tmB128, &tmB256};
+  if (warp == kWarpProducer && lane == 0) {
+    const CUtensorMap* maps[7] = {&tmA0, &tmA1, &tmB16, &tmB32, &tmB64, &tmB128, &tmB256};
 #pragma unroll
-    for (int m = 0; m < 6; ++m)
+    for (int m = 0; m < 7; ++m)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps[m])) : "memory");
     for (int s = 0; s < kDStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -179,187 +208,198 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc_pair(&tmem_slot, 2 * kAccCols);
+  if (warp == kWarpAlloc) tmem_alloc_pair(&tmem_slot, 2 * kAccCols);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tbase = tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kWarpProducer) {
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int it = 0;
-      for (int j = j0; j < j1; ++j) {
-        const DenseTile tl = a.tiles[j];
-        const int half = tl.nlen >> 1;
-        const int arow = tl.m_blk * 256 + (int)cta * 128;
-        const int brow = tl.n0 + (int)cta * half;
-        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
-          const int s = it % kDStages;
-          mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
-#ifdef NMFA_DBG_TRACE
-          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 0) * 256 + it] = clock64();
-#endif
-          const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
-          if (cta == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
-          uint8_t* st = smem + (size_t)s * kDStageBytes;
-          tma2d_pair(smem_u32(st), &tmA, 0, (int)(kb * a.Rp + arow) * 2, fb);
-          int off = 0;  // rows
-#pragma unroll
-          for (int b = 4; b >= 0; --b) {
-            const int rows = 8 << b;
-            if (half & rows) {
-              const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
-                                    : b == 1 ? &tmB32 : &tmB16;
-              tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
-                         (kb * a.np + brow + off) * 2, fb);
-              off += rows;
-            }
+      for (int ph = 0; ph < n_phases; ++ph) {
+        const int t = a.t_begin + ph;
+        const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
+        for (int j = j0; j < j1; ++j) {
+          const DenseTile tl = a.tiles[j];
+          if (ph > 0) {  // rows of block m for sweep t were written by sweep t-1's epilogues
+            const unsigned need = (unsigned)ph * 2u * (unsigned)a.m_tiles[tl.m_blk];
+            while (ld_acquire_gpu(a.ready + tl.m_blk) < need) __nanosleep(32);
+            fence_proxy_async_global();
           }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------- MMA issuer (leader CTA) -------------------------
-    if (cta == 0 && lane == 0) {
-      int it = 0;
-      for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
-        const DenseTile tl = a.tiles[j];
-        const int slot = jj & 1, use = jj >> 1;
-        mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
-#ifdef NMFA_DBG_TRACE
-        if (a.trace && blockIdx.x < 2 && jj < 256) a.trace[(blockIdx.x * 4 + 3) * 256 + jj] = clock64();
-#endif
-        tc_fence_after();
-        const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
-        const uint32_t d = tbase + (uint32_t)slot * kAccCols;
-        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
-          const int s = it % kDStages;
-#ifdef NMFA_DBG_TRACE
-          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 1) * 256 + it] = clock64();
-#endif
-          mbar_wait(&full_bar[s], (it / kDStages) & 1);
-#ifdef NMFA_DBG_TRACE
-          if (a.trace && blockIdx.x < 2 && it < 256) a.trace[(blockIdx.x * 4 + 2) * 256 + it] = clock64();
-#endif
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + (size_t)s * kDStageBytes);
-          const uint32_t sb = sa + kATile;
-          const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : kBK / 16;
-          for (int ks = 0; ks < nsub; ++ks) {
-            mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 2048),
-                     make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (kb | ks) ? 1u : 0u);
-          }
-          commit_pair_mc(&empty_bar[s]);
-        }
-        commit_pair_mc(&tfull_bar[slot]);
-      }
-    }
-  } else if (warp >= 4) {
-    // ------------------------- fused NMFA epilogue -------------------------
-    // State per (replica r, spin i): hi = fp16(s) lives in the operand image
-    // the TMA is reading this step (a_cur), lo = fp16(s - hi) in a second image
-    // of the same layout, so s = hi + lo carries ~22 bits and the whole
-    // per-step working set (2 images + lo + J) stays L2-resident.
-    const int e = warp - 4, quarter = e & 3, hpart = e >> 2;  // 4 lane quarters x 4 column parts
-    const int row = 32 * quarter + lane;
-    const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
-    const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
-    const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
-    const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
-    for (int j = j0, jj = 0; j < j1; ++j, ++jj) {
-      const DenseTile tl = a.tiles[j];
-      const int slot = jj & 1, use = jj >> 1;
-      const long long r = (long long)tl.m_blk * 256 + (long long)cta * 128 + row;
-      const bool valid = r < a.R;
-      const unsigned long long key = a.key_base + (unsigned long long)r;
-      const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
-      const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
-      mbar_wait(&tfull_bar[slot], use & 1);
-      tc_fence_after();
-      const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
-      const int nch = tl.nlen >> 4;
-      if constexpr (kEnergy) {
-        // a_cur holds the +-1 configuration written by the last anneal step
-        double e_pair = 0.0, e_field = 0.0;
-        for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
-          const int i0 = tl.n0 + 16 * c;
-          float acc[16];
-          tmem_ld16(tacc + 16 * c, acc);
-          const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
-          const uint4 c0 = *reinterpret_cast<const uint4*>(a.a_cur + off);
-          const uint4 c1 = *reinterpret_cast<const uint4*>(a.a_cur + off + 128);
-          float cs[16];
-          unpack_half8(c0, cs);
-          unpack_half8(c1, cs + 8);
-          tmem_wait_ld();
-          const int nvalid = valid ? min(16, a.n - i0) : 0;
+          const int half = tl.nlen >> 1;
+          const int arow = tl.m_blk * 256 + (int)cta * 128;
+          const int brow = tl.n0 + (int)cta * half;
+          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+            const int s = it % kDStages;
+            mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+            const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
+            if (cta == 0)
+              mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
+            uint8_t* st = smem + (size_t)s * kDStageBytes;
+            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb);
+            int off = 0;  // rows
 #pragma unroll
-          for (int cc = 0; cc < 16; ++cc) {
-            if (cc < nvalid) {
-              e_pair += (double)(cs[cc] * acc[cc]);                // c_i (J c)_i, exact integers
-              const double hv = __ldg(a.h + i0 + cc);
-              e_field += cs[cc] < 0.f ? -hv : hv;
-            }
-          }
-        }
-        if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
-      } else {
-        const bool extra = valid && (a.s_hist != nullptr || a.last);
-        for (int c = hpart; c < nch; c += kDEpiWarps / 4) {
-          const int i0 = tl.n0 + 16 * c;
-          float acc[16], ms[16], lo[16];
-          tmem_ld16(tacc + 16 * c, acc);
-          const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
-          const uint4 h0 = *reinterpret_cast<const uint4*>(a.a_cur + off);
-          const uint4 h1 = *reinterpret_cast<const uint4*>(a.a_cur + off + 128);
-          const uint4 l0 = *reinterpret_cast<const uint4*>(a.lo + off);
-          const uint4 l1 = *reinterpret_cast<const uint4*>(a.lo + off + 128);
-          unpack_half8(h0, ms);
-          unpack_half8(h1, ms + 8);
-          unpack_half8(l0, lo);
-          unpack_half8(l1, lo + 8);
-#pragma unroll
-          for (int cc = 0; cc < 16; ++cc) ms[cc] += lo[cc];
-          tmem_wait_ld();
-          const int nvalid = valid ? min(16, a.n - i0) : 0;
-          const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + a.t) * a.n + i0 : nullptr;
-          update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
-                              (uint32_t)(i0 / 4), (uint32_t)a.t, a.sigma, a.inv_t, a.alpha, a.oma);
-          // split s -> (hi, lo); the last step writes the +-1 configuration for the energy pass
-          uint4 hv[2], lv[2];
-          split_half16(ms, hv, lv, a.last != 0);
-          *reinterpret_cast<uint4*>(a.a_next + off) = hv[0];
-          *reinterpret_cast<uint4*>(a.a_next + off + 128) = hv[1];
-          *reinterpret_cast<uint4*>(a.lo + off) = lv[0];
-          *reinterpret_cast<uint4*>(a.lo + off + 128) = lv[1];
-          if (extra) {
-            if (a.s_hist) {
-              float* hrow = a.s_hist + ((long long)r * a.t_f + a.t) * a.n + i0;
-#pragma unroll
-              for (int cc = 0; cc < 16; ++cc)
-                if (cc < nvalid) hrow[cc] = ms[cc];
-            }
-            if (a.last) {
-#pragma unroll
-              for (int cc = 0; cc < 16; ++cc) {
-                if (cc < nvalid) {
-                  a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181
-                  if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
-                }
+            for (int b = 4; b >= 0; --b) {
+              const int rows = 8 << b;
+              if (half & rows) {
+                const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
+                                      : b == 1 ? &tmB32 : &tmB16;
+                tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
+                           (kb * a.np + brow + off) * 2, fb);
+                off += rows;
               }
             }
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
+    }
+  } else if (warp == kWarpMma) {
+    // ------------------------- MMA issuer (leader CTA) -------------------------
+    if (cta == 0 && lane == 0) {
+      int it = 0, jj = 0;
+      for (int ph = 0; ph < n_phases; ++ph) {
+        for (int j = j0; j < j1; ++j, ++jj) {
+          const DenseTile tl = a.tiles[j];
+          const int slot = jj & 1, use = jj >> 1;
+          mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
+          const uint32_t d = tbase + (uint32_t)slot * kAccCols;
+          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+            const int s = it % kDStages;
+            mbar_wait(&full_bar[s], (it / kDStages) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + (size_t)s * kDStageBytes);
+            const uint32_t sb = sa + kATile;
+            const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : kBK / 16;
+            for (int ks = 0; ks < nsub; ++ks) {
+              mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 2048),
+                       make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (kb | ks) ? 1u : 0u);
+            }
+            commit_pair_mc(&empty_bar[s]);
+          }
+          commit_pair_mc(&tfull_bar[slot]);
+        }
+      }
+    }
+  } else if (warp < kDEpiWarps) {
+    // ------------------------- fused NMFA epilogue -------------------------
+    // State per (replica r, spin i): hi = fp16(s) lives in the operand image
+    // the TMA reads this sweep, lo = fp16(s - hi) in a second image of the same
+    // layout, so s = hi + lo carries ~22 bits and the per-sweep working set
+    // (2 images + lo + J) is ~104 MB at K2000 / 8192 reads.
+    const int e = warp, quarter = e & 3, hpart = e >> 2;  // lane quarter x column part
+    constexpr int kStep = kDEpiWarps / 4;
+    const int row = 32 * quarter + lane;
+    const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
+    const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
+    const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
+    const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+    int jj = 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+      const int t = a.t_begin + ph;
+      const bool energy_phase = t >= a.t_end;
+      const bool last = (t == a.t_f - 1);
+      const float inv_t = energy_phase ? 0.f : __ldg(a.inv_temp + t);
+      const uint8_t* a_cur = (t & 1) ? a.img1 : a.img0;
+      uint8_t* a_next = (t & 1) ? a.img0 : a.img1;
+      for (int j = j0; j < j1; ++j, ++jj) {
+        const DenseTile tl = a.tiles[j];
+        const int slot = jj & 1, use = jj >> 1;
+        const long long r = (long long)tl.m_blk * 256 + (long long)cta * 128 + row;
+        const bool valid = r < a.R;
+        const unsigned long long key = a.key_base + (unsigned long long)r;
+        const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
+        const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
+        mbar_wait(&tfull_bar[slot], use & 1);
+        tc_fence_after();
+        const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
+        const int nch = tl.nlen >> 4;
+        if (energy_phase) {
+          // a_cur holds the +-1 configuration written by the last sweep
+          double e_pair = 0.0, e_field = 0.0;
+          for (int c = hpart; c < nch; c += kStep) {
+            const int i0 = tl.n0 + 16 * c;
+            float acc[16];
+            tmem_ld16(tacc + 16 * c, acc);
+            const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
+            float cs[16];
+            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), cs);
+            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off + 128), cs + 8);
+            tmem_wait_ld();
+            const int nvalid = valid ? min(16, a.n - i0) : 0;
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+              if (cc < nvalid) {
+                e_pair += (double)(cs[cc] * acc[cc]);        // c_i (J c)_i, exact integers
+                const double hv = __ldg(a.h + i0 + cc);
+                e_field += cs[cc] < 0.f ? -hv : hv;
+              }
+            }
+          }
+          if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
+        } else {
+          const bool extra = valid && (a.s_hist != nullptr || last);
+          for (int c = hpart; c < nch; c += kStep) {
+            const int i0 = tl.n0 + 16 * c;
+            const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
+            float acc[16], ms[16], lo[16];
+            tmem_ld16(tacc + 16 * c, acc);
+            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), ms);
+            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off + 128), ms + 8);
+            unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off), lo);
+            unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off + 128), lo + 8);
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) ms[cc] += lo[cc];
+            tmem_wait_ld();
+            const int nvalid = valid ? min(16, a.n - i0) : 0;
+            const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + t) * a.n + i0 : nullptr;
+            update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
+                                (uint32_t)(i0 / 4), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+            // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
+            uint4 hv[2], lv[2];
+            split_half16(ms, hv, lv, last);
+            *reinterpret_cast<uint4*>(a_next + off) = hv[0];
+            *reinterpret_cast<uint4*>(a_next + off + 128) = hv[1];
+            *reinterpret_cast<uint4*>(a.lo + off) = lv[0];
+            *reinterpret_cast<uint4*>(a.lo + off + 128) = lv[1];
+            if (extra) {
+              if (a.s_hist) {
+                float* hrow = a.s_hist + ((long long)r * a.t_f + t) * a.n + i0;
+#pragma unroll
+                for (int cc = 0; cc < 16; ++cc)
+                  if (cc < nvalid) hrow[cc] = ms[cc];
+              }
+              if (last) {
+#pragma unroll
+                for (int cc = 0; cc < 16; ++cc) {
+                  if (cc < nvalid) {
+                    a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181
+                    if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
+                  }
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
+        // publish this CTA's rows of the tile for the next sweep of block m
+        asm volatile("bar.sync 1, %0;" ::"n"(kDEpiWarps * 32) : "memory");
+        if (e == 0 && lane == 0) {
+          __threadfence();
+          fence_proxy_async_global();
+          atomicAdd(a.ready + tl.m_blk, 1u);
+        }
+      }
     }
   }
   tc_fence_before();
   cluster_sync_all();
-  if (warp == 2) {
+  if (warp == kWarpAlloc) {
     tc_fence_after();
     tmem_dealloc_pair(tbase, 2 * kAccCols);
   }
@@ -444,6 +484,8 @@ void dense_plan_free(nmfa_plan* pl) {
   if (ds->a_img[1]) cudaFree(ds->a_img[1]);
   if (ds->d_tiles) cudaFree(ds->d_tiles);
   if (ds->d_tile_off) cudaFree(ds->d_tile_off);
+  if (ds->d_m_tiles) cudaFree(ds->d_m_tiles);
+  if (ds->d_ready) cudaFree(ds->d_ready);
   delete ds;
   pl->dense = nullptr;
 }
@@ -494,6 +536,12 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_tile_off, off.size() * sizeof(int)));
   NMFA_CUDA_TRY(
       cudaMemcpy(ds->d_tile_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  ds->n_mblk = (int)mb;
+  std::vector<int> m_tiles(mb, 0);
+  for (const DenseTile& t : tiles) m_tiles[t.m_blk]++;
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_m_tiles, mb * sizeof(int)));
+  NMFA_CUDA_TRY(cudaMemcpy(ds->d_m_tiles, m_tiles.data(), mb * sizeof(int), cudaMemcpyHostToDevice));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_ready, mb * sizeof(unsigned)));
 
   int err;
   for (int b = 0; b < 2; ++b)
@@ -502,11 +550,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   for (int b = 0; b < 5; ++b)
     if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np * 2, 16u << b)))
       return err;
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false, false>,
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_anneal_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<true, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_step_kernel<false, true>,
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_anneal_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
   return NMFA_OK;
 }
@@ -524,80 +570,57 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
       ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
   NMFA_LAUNCH_CHECK();
+  *energy_done = energy && dense_energy_exact(p);
+  if (*energy_done) NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
+  NMFA_CUDA_TRY(cudaMemsetAsync(ds->d_ready, 0, sizeof(unsigned) * ds->n_mblk, st));
   DenseStepArgs a{};
   a.tiles = ds->d_tiles;
   a.tile_off = ds->d_tile_off;
+  a.m_tiles = ds->d_m_tiles;
+  a.ready = ds->d_ready;
   a.kblocks = ds->kblocks;
   a.k_last_sub = ds->k_last_sub;
   a.n = (int)p->n;
   a.np = ds->np;
   a.R = pl->R;
   a.Rp = ds->Rp;
+  a.t_begin = 0;
+  a.t_end = pl->t_f;
   a.t_f = pl->t_f;
+  a.energy_pass = *energy_done ? 1 : 0;
   a.alpha = pl->alpha;
   a.oma = pl->oma;
   a.sigma = pl->sigma;
+  a.inv_temp = pl->d_inv_temp;
   a.invn = p->d_invn;
   a.hn = p->d_hn;
+  a.img0 = ds->a_img[0];
+  a.img1 = ds->a_img[1];
   a.lo = ds->lo_img;
   a.key_base = key_base;
   a.noise = noise;
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
-#ifdef NMFA_DBG_TRACE
-  static unsigned long long* trace = nullptr;
-  if (!trace) cudaMallocManaged(&trace, 16 * 256 * 8);
-  a.trace = trace;
-#endif
-  for (int t = 0; t < pl->t_f; ++t) {
-    a.t = t;
-    a.inv_t = pl->h_inv_temp[t];
-    a.last = (t == pl->t_f - 1);
-    a.a_cur = ds->a_img[t & 1];
-    a.a_next = ds->a_img[(t + 1) & 1];
-    auto kern = noise ? dense_step_kernel<true, false> : dense_step_kernel<false, false>;
-    kern<<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
-        ds->tmA[t & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
-    NMFA_LAUNCH_CHECK();
-  }
-#ifdef NMFA_DBG_TRACE
-  cudaStreamSynchronize(st);
-  {
-    FILE* f = fopen("gpurun_out/dense_trace.txt", "w");
-    for (int b = 0; b < 2; ++b)
-      for (int it = 0; it < 256; ++it)
-        fprintf(f, "%d %d %llu %llu %llu %llu\n", b, it, trace[(b * 4 + 0) * 256 + it],
-                trace[(b * 4 + 1) * 256 + it], trace[(b * 4 + 2) * 256 + it],
-                trace[(b * 4 + 3) * 256 + it]);
-    fclose(f);
-    f = fopen("gpurun_out/dense_trace_epi.txt", "w");
-    for (int e = 0; e < 16; ++e)
-      for (int jj = 0; jj < 4; ++jj) {
-        fprintf(f, "%d %d", e, jj);
-        for (int k = 0; k < 8; ++k) fprintf(f, " %llu", trace[8 * 256 + (e * 4 + jj) * 8 + k]);
-        fprintf(f, "\n");
-      }
-    fclose(f);
-  }
-#endif
-  add_launches(1 + pl->t_f);
-  *energy_done = false;
-  if (energy && dense_energy_exact(p)) {
-    // one more GEMM pass over the +-1 configuration image (written by the last step)
-    NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
-    a.energy = energy;
-    a.h = p->d_h;
-    a.half_scale = 0.5 * p->j_scale;
-    a.last = 0;
-    a.t = pl->t_f;
-    a.a_cur = ds->a_img[pl->t_f & 1];
-    dense_step_kernel<false, true><<<2 * ds->pairs, kDThreads, kDSmemBytes, st>>>(
-        ds->tmA[pl->t_f & 1], ds->tmB[0], ds->tmB[1], ds->tmB[2], ds->tmB[3], ds->tmB[4], a);
-    NMFA_LAUNCH_CHECK();
-    add_launches(1);
-    *energy_done = true;
-  }
+  a.energy = energy;
+  a.h = p->d_h;
+  a.half_scale = 0.5 * p->j_scale;
+  // one persistent launch for every sweep; all clusters must be co-resident
+  // (the readiness spin-waits cross CTAs), which the cooperative attribute asserts
+  cudaLaunchConfig_t cfgl{};
+  cfgl.gridDim = dim3(2 * ds->pairs);
+  cfgl.blockDim = dim3(kDThreads);
+  cfgl.dynamicSmemBytes = kDSmemBytes;
+  cfgl.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfgl.attrs = attr;
+  cfgl.numAttrs = 1;
+  auto kern = noise ? dense_anneal_kernel<true> : dense_anneal_kernel<false>;
+  NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1],
+                                   ds->tmB[2], ds->tmB[3], ds->tmB[4], a));
+  add_launches(2);
   return NMFA_OK;
 }
 

@@ -67,21 +67,14 @@ __device__ __forceinline__ float nmfa_update(float acc, float inv_norm, float h_
 // ---------------------------------------------------------------------------
 struct uint4_ { uint32_t x, y, z, w; };
 
-// Per-replica Philox round keys (the key is fixed for a replica, so the
-// schedule is computed once per replica and reused for every counter).
+// Per-replica Philox key.  Round keys k + i*W are formed inline (one add with
+// an immediate per round): holding all 20 round keys in registers costs more
+// (register pressure in the 16-warp epilogue) than the adds.
 struct PhiloxKey {
-  uint32_t k0[10], k1[10];
+  uint32_t k0, k1;
 };
 
-__device__ __forceinline__ PhiloxKey philox_schedule(uint32_t k0, uint32_t k1) {
-  PhiloxKey K;
-#pragma unroll
-  for (int i = 0; i < 10; ++i) {
-    K.k0[i] = k0 + (uint32_t)i * 0x9E3779B9u;
-    K.k1[i] = k1 + (uint32_t)i * 0xBB67AE85u;
-  }
-  return K;
-}
+__device__ __forceinline__ PhiloxKey philox_schedule(uint32_t k0, uint32_t k1) { return {k0, k1}; }
 
 __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
                                                 uint32_t c3, const PhiloxKey& K) {
@@ -90,8 +83,8 @@ __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32
   for (int i = 0; i < 10; ++i) {
     const uint64_t p0 = (uint64_t)M0 * c0;  // IMAD.WIDE.U32
     const uint64_t p1 = (uint64_t)M1 * c2;
-    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k0[i];
-    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k1[i];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ (K.k0 + (uint32_t)i * 0x9E3779B9u);
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ (K.k1 + (uint32_t)i * 0xBB67AE85u);
     c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
   }
   return {c0, c1, c2, c3};
