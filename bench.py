@@ -281,7 +281,10 @@ def run_ours(args):
     en_h = torch.empty(R, dtype=torch.float64).pin_memory()
     temps_h = torch.from_numpy(np.ascontiguousarray(temps)).pin_memory()
     handle = p.device_handle(local).handle
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 5))
+    _native.check(lib.nmfa_anneal_host(handle, R, t_f, _native.ptr(temps_h), params.alpha,
+                                       params.sigma, params.seed, r0, _native.ptr(cfg_h),
+                                       _native.ptr(en_h)))  # warm-up: builds the cached plan
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()

@@ -405,19 +405,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   }
 }
 
-// A image 0 (hi) and the lo image from s0 (or zeros); padding stays zero.
+// A image 0 (hi) and the lo image from s0: one thread per (replica, 8-spin
+// core row) writes one 16-byte chunk of each image (padding stays zero).
 __global__ void dense_init_kernel(uint8_t* a_img, uint8_t* lo_img, const float* s0, int n, int kp,
                                   long long R, long long Rp) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)kp * Rp) return;
+  if (e >= (long long)(kp / 8) * Rp) return;
   const long long r = e % Rp;
-  const int i = (int)(e / Rp);
-  const float v = (s0 && r < R && i < n) ? s0[r * n + i] : 0.f;
-  const long long off = (long long)(i >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
-                        (r & 7) * 16 + (i & 7) * 2;
-  const __half h = __float2half_rn(v);
-  *reinterpret_cast<__half*>(a_img + off) = h;
-  *reinterpret_cast<__half*>(lo_img + off) = __float2half_rn(v - __half2float(h));
+  const int i0 = (int)(e / Rp) * 8;
+  float v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = (r < R && i0 + k < n) ? s0[r * n + i0 + k] : 0.f;
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const __half2 hh = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(v[2 * k] - hf.x, v[2 * k + 1] - hf.y);
+    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[k] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  const long long off = (long long)(i0 >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i0 & 127) >> 3) * 128 +
+                        (r & 7) * 16;
+  *reinterpret_cast<uint4*>(a_img + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo_img + off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -566,10 +577,16 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
     set_error("dense plan state missing");
     return NMFA_ERR_STATE;
   }
-  const long long tot = (long long)ds->kp * ds->Rp;
-  dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-      ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
-  NMFA_LAUNCH_CHECK();
+  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  if (s0) {
+    const long long tot = (long long)(ds->kp / 8) * ds->Rp;
+    dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
+    NMFA_LAUNCH_CHECK();
+  } else {  // S(0) = 0 (solver.py:200-201)
+    NMFA_CUDA_TRY(cudaMemsetAsync(ds->a_img[0], 0, img_bytes, st));
+    NMFA_CUDA_TRY(cudaMemsetAsync(ds->lo_img, 0, img_bytes, st));
+  }
   *energy_done = energy && dense_energy_exact(p);
   if (*energy_done) NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
   NMFA_CUDA_TRY(cudaMemsetAsync(ds->d_ready, 0, sizeof(unsigned) * ds->n_mblk, st));
