@@ -1,7 +1,10 @@
 // C-ABI layer: problem construction (problem.py:25-116 restated in C++),
 // plans, dispatch to the kernel paths, errors.  See include/nmfa_b200.h.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -47,6 +50,9 @@ int64_t nmfa_last_launch_count(void) { return g_launches; }
 int nmfa_problem_destroy(nmfa_problem_t* p) {
   if (!p) return NMFA_OK;
   if (p->cached_plan) nmfa_plan_destroy(p->cached_plan);
+  if (p->host_cfg) cudaFree(p->host_cfg);
+  if (p->host_e) cudaFree(p->host_e);
+  if (p->host_stream) cudaStreamDestroy(p->host_stream);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
@@ -457,7 +463,13 @@ int nmfa_anneal(const nmfa_problem_t* cp, int64_t R, int32_t t_f, const double* 
     p->cached_alpha = alpha;
     p->cached_sigma = sigma;
   }
+  static const bool timing = getenv("NMFA_TIMING") != nullptr;
+  const auto ta = std::chrono::steady_clock::now();
   int err = nmfa_plan_run(pl, seed, r0, noise, s0, cfg, energy, s_out, s_hist, e_hist, stream);
+  const auto tb = std::chrono::steady_clock::now();
+  if (timing)
+    fprintf(stderr, "nmfa_anneal: cache %s, enqueue %.3f ms\n", hit ? "hit" : "miss",
+            std::chrono::duration<double, std::milli>(tb - ta).count());
   if (!err && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
     set_error(std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
     err = NMFA_ERR_CUDA;
@@ -470,35 +482,52 @@ int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
                      double* energy_host) {
   if (!p || !cfg_host) return arg_error("NULL argument");
   if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
+  static const bool timing = getenv("NMFA_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
-  int8_t* d_cfg = nullptr;
-  double* d_e = nullptr;
-  cudaStream_t st = nullptr;
+  auto* mp = const_cast<nmfa_problem*>(p);
   int err = NMFA_OK;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMallocAsync(&d_cfg, (size_t)R * p->n, st) != cudaSuccess ||
-      cudaMallocAsync(&d_e, (size_t)R * 8, st) != cudaSuccess) {
-    set_error("out of device memory");
-    err = NMFA_ERR_CUDA;
+  {
+    // device result buffers and the stream are cached on the problem handle
+    std::lock_guard<std::mutex> lock(mp->cache_mu);
+    if (!mp->host_stream && cudaStreamCreateWithFlags(&mp->host_stream, cudaStreamNonBlocking))
+      err = NMFA_ERR_CUDA;
+    if (!err && mp->host_cap < R) {
+      if (mp->host_cfg) cudaFree(mp->host_cfg);
+      if (mp->host_e) cudaFree(mp->host_e);
+      mp->host_cfg = nullptr;
+      mp->host_e = nullptr;
+      if (cudaMalloc(&mp->host_cfg, (size_t)R * p->n) || cudaMalloc(&mp->host_e, (size_t)R * 8))
+        err = NMFA_ERR_CUDA;
+      else
+        mp->host_cap = R;
+    }
   }
-  if (!err)
-    err = nmfa_anneal(p, R, t_f, temps, alpha, sigma, seed, r0, nullptr, nullptr, d_cfg,
-                      energy_host ? d_e : nullptr, nullptr, nullptr, nullptr, st);
-  if (!err && (cudaMemcpyAsync(cfg_host, d_cfg, (size_t)R * p->n, cudaMemcpyDeviceToHost, st) ||
-               (energy_host && cudaMemcpyAsync(energy_host, d_e, (size_t)R * 8,
+  if (err) {
+    set_error("out of device memory / stream creation failed");
+    cudaSetDevice(prev);
+    return err;
+  }
+  cudaStream_t st = mp->host_stream;
+  const auto t1 = now();
+  err = nmfa_anneal(p, R, t_f, temps, alpha, sigma, seed, r0, nullptr, nullptr, mp->host_cfg,
+                    energy_host ? mp->host_e : nullptr, nullptr, nullptr, nullptr, st);
+  const auto t2 = now();
+  if (!err && (cudaMemcpyAsync(cfg_host, mp->host_cfg, (size_t)R * p->n, cudaMemcpyDeviceToHost, st) ||
+               (energy_host && cudaMemcpyAsync(energy_host, mp->host_e, (size_t)R * 8,
                                                cudaMemcpyDeviceToHost, st)) ||
                cudaStreamSynchronize(st))) {
     set_error("device to host copy failed");
     err = NMFA_ERR_CUDA;
   }
-  if (d_cfg) cudaFreeAsync(d_cfg, st);
-  if (d_e) cudaFreeAsync(d_e, st);
-  if (st) {
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
-  }
+  const auto t3 = now();
+  if (timing)
+    fprintf(stderr, "nmfa_anneal_host: setup %.3f ms, anneal %.3f ms, d2h %.3f ms\n", ms(t0, t1),
+            ms(t1, t2), ms(t2, t3));
   cudaSetDevice(prev);
   return err;
 }

@@ -69,6 +69,11 @@ struct nmfa_problem {
   nmfa_plan* cached_plan = nullptr;
   std::vector<double> cached_temps;
   double cached_alpha = -1.0, cached_sigma = -1.0;
+  // nmfa_anneal_host: device result buffers + stream
+  cudaStream_t host_stream = nullptr;
+  int8_t* host_cfg = nullptr;
+  double* host_e = nullptr;
+  int64_t host_cap = 0;
 };
 
 struct nmfa_plan {
