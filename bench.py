@@ -152,6 +152,60 @@ def cpu_reference(workload, sample_runs=None, threads=None):
             "wall_s": wall}
 
 
+def measure_tts_sk100(nb, dev, skip_cpu=False):
+    """TTS99 on the 100-spin SK instance (the metric's second half).
+
+    GPU: one batch of 37,888 reads (2 per SM-resident CTA of 128), tau = batch
+    time / reads, p = P(E <= -730), -730 being the best of 10,000 reference
+    runs (tests/golden/stats.npz).  CPU: tau of the jitted reference port on
+    the host cores; p from the reference's own 10,000-run statistics.
+    """
+    import math
+
+    import numpy as np
+    import torch
+
+    e_ref = -730.0
+    p = nb.gen_sk(100, 0)
+    R = 37888
+    params = nb.NmfaParams(t_f=1000, seed=12345)
+    nb.sample(p, params, R, device=dev.index)                     # warm (plan cache)
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev[0].record()
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=777), R, device=dev.index)
+    ev[1].record()
+    torch.cuda.synchronize(dev)
+    wall = ev[0].elapsed_time(ev[1]) * 1e-3
+    e = res.energies.cpu().numpy()
+    k = int(np.count_nonzero(e <= e_ref + 1e-9))
+    pg = k / R
+    tau = wall / R
+    out = {"instance": "gen_sk(100,0), t_f=1000, E_ref=-730 (best of 10k reference runs)",
+           "gpu": {"reads": R, "p": pg, "tau_s": tau,
+                   "tts99_s": tau * math.log(0.01) / math.log(1 - pg) if 0 < pg < 0.99 else None}}
+    try:
+        golden = np.load(os.path.join(REPO, "tests", "golden", "stats.npz"))
+        pref = float(np.mean(golden["sk100_E"] <= e_ref + 1e-9))
+        out["reference_p"] = pref
+    except OSError:
+        pref = None
+    if not skip_cpu and pref:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import nmfa_oracle as O
+
+        op = O.problem_from_edges(100, p.edges_i, p.edges_j, p.edge_weights)
+        threads = os.cpu_count() or 1
+        O.batch(op, 0, threads, t_f=50, threads=threads)
+        runs = 32 * threads
+        t0 = time.perf_counter()
+        O.batch(op, 0, runs, t_f=1000, threads=threads)
+        tau_c = (time.perf_counter() - t0) / runs
+        out["cpu_reference"] = {"runs": runs, "threads": threads, "tau_s": tau_c, "p": pref,
+                                "tts99_s": tau_c * math.log(0.01) / math.log(1 - pref)}
+    return out
+
+
 def run_reference(args):
     world, rank, _ = dist_init()
     if rank != 0:
@@ -299,6 +353,10 @@ def run_ours(args):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_value = world * n * R * t_f * e2e_steps / float(et.item())
 
+    tts = None
+    if rank == 0 and not args.no_tts:
+        tts = measure_tts_sk100(nb, dev, args.no_cpu_baseline)
+
     cpu_bl = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference(args.workload, sample_runs=args.ref_runs)
@@ -324,6 +382,7 @@ def run_ours(args):
                     "api": "nmfa_anneal_host (C ABI, host buffers)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "tts99_sk100": tts,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -342,6 +401,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-runs", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tts", action="store_true", help="skip the SK100 TTS99 side measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
