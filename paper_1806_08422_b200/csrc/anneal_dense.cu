@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <numeric>
 
 #include "common.cuh"
 #include "internal.h"
@@ -64,8 +65,9 @@ struct DenseState {
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
-  int* d_m_tiles = nullptr;       // tiles per replica block
-  unsigned* d_ready = nullptr;    // per replica block readiness counters
+  int* d_korder = nullptr;        // per replica block: static k-slice order
+  unsigned* d_kneed = nullptr;    // per (block, k-slice): spins published per sweep (x2 CTAs)
+  unsigned* d_ready = nullptr;    // per (block, k-slice): spins published this launch
   int n_mblk = 0;
   CUtensorMap tmA[2];
   CUtensorMap tmB[5];  // box lines 16, 32, 64, 128, 256 (= 8..128 rows)
@@ -74,8 +76,9 @@ struct DenseState {
 struct DenseStepArgs {
   const DenseTile* tiles;
   const int* tile_off;
-  const int* m_tiles;      // tiles per replica block (whole schedule)
-  unsigned* ready;         // per replica block: (CTA, tile) epilogues completed this launch
+  const int* korder;       // [m][kblocks] static k-slice order of block m's tiles
+  const unsigned* kneed;   // [m][kblocks] spins a sweep publishes into the slice (both CTAs)
+  unsigned* ready;         // [m][kblocks] spins published so far this launch
   int kblocks, k_last_sub;
   int n, np;
   long long R, Rp;
@@ -169,8 +172,11 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // mode: the A operand is then the +-1 configuration written by the last sweep
 // and the epilogue reduces E_r = 1/2 c_r.(J c_r) + h.c_r exactly (integer J,
 // |J c| < 2^24).  Sweep t+1 of replica block m may start once every (CTA, tile)
-// epilogue of block m for sweep t has published its rows (`ready[m]`), which is
-// the only inter-CTA dependency: replica blocks are independent.
+// epilogue of block m for sweep t has published its rows, tracked per
+// 128-spin k-slice (`ready[m][kb]`, counted in spins): the next sweep's MMAs
+// start on the slices that finished first (a static, deterministic order per
+// block, so results do not depend on timing) while the previous sweep's last
+// epilogues are still running.  Replica blocks are independent.
 template <bool kInjected>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_anneal_kernel(const __grid_constant__ CUtensorMap tmA0,
@@ -223,15 +229,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
         for (int j = j0; j < j1; ++j) {
           const DenseTile tl = a.tiles[j];
-          if (ph > 0) {  // rows of block m for sweep t were written by sweep t-1's epilogues
-            const unsigned need = (unsigned)ph * 2u * (unsigned)a.m_tiles[tl.m_blk];
-            while (ld_acquire_gpu(a.ready + tl.m_blk) < need) __nanosleep(32);
-            fence_proxy_async_global();
-          }
           const int half = tl.nlen >> 1;
           const int arow = tl.m_blk * 256 + (int)cta * 128;
           const int brow = tl.n0 + (int)cta * half;
-          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const int* kord = a.korder + tl.m_blk * a.kblocks;
+          for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
+            const int kb = kord[ki];
+            if (ph > 0) {  // slice kb of block m for sweep t was written by sweep t-1
+              const int q = tl.m_blk * a.kblocks + kb;
+              const unsigned need = (unsigned)ph * a.kneed[q];
+              if (ld_acquire_gpu(a.ready + q) < need) {
+                while (ld_acquire_gpu(a.ready + q) < need) __nanosleep(20);
+              }
+              fence_proxy_async_global();
+            }
             const int s = it % kDStages;
             mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
             const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
@@ -267,7 +278,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           tc_fence_after();
           const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
           const uint32_t d = tbase + (uint32_t)slot * kAccCols;
-          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const int* kord = a.korder + tl.m_blk * a.kblocks;
+          for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
+            const int kb = kord[ki];
             const int s = it % kDStages;
             mbar_wait(&full_bar[s], (it / kDStages) & 1);
             tc_fence_after();
@@ -276,7 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : kBK / 16;
             for (int ks = 0; ks < nsub; ++ks) {
               mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 2048),
-                       make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (kb | ks) ? 1u : 0u);
+                       make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (ki | ks) ? 1u : 0u);
             }
             commit_pair_mc(&empty_bar[s]);
           }
@@ -392,7 +405,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         if (e == 0 && lane == 0) {
           __threadfence();
           fence_proxy_async_global();
-          atomicAdd(a.ready + tl.m_blk, 1u);
+          for (int kb = tl.n0 >> 7; kb <= (tl.n0 + tl.nlen - 1) >> 7; ++kb) {
+            const int lo_s = max(tl.n0, kb * 128), hi_s = min(tl.n0 + tl.nlen, kb * 128 + 128);
+            atomicAdd(a.ready + tl.m_blk * a.kblocks + kb, (unsigned)(hi_s - lo_s));
+          }
         }
       }
     }
@@ -495,7 +511,8 @@ void dense_plan_free(nmfa_plan* pl) {
   if (ds->a_img[1]) cudaFree(ds->a_img[1]);
   if (ds->d_tiles) cudaFree(ds->d_tiles);
   if (ds->d_tile_off) cudaFree(ds->d_tile_off);
-  if (ds->d_m_tiles) cudaFree(ds->d_m_tiles);
+  if (ds->d_korder) cudaFree(ds->d_korder);
+  if (ds->d_kneed) cudaFree(ds->d_kneed);
   if (ds->d_ready) cudaFree(ds->d_ready);
   delete ds;
   pl->dense = nullptr;
@@ -548,11 +565,36 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(
       cudaMemcpy(ds->d_tile_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
   ds->n_mblk = (int)mb;
-  std::vector<int> m_tiles(mb, 0);
-  for (const DenseTile& t : tiles) m_tiles[t.m_blk]++;
-  NMFA_CUDA_TRY(cudaMalloc(&ds->d_m_tiles, mb * sizeof(int)));
-  NMFA_CUDA_TRY(cudaMemcpy(ds->d_m_tiles, m_tiles.data(), mb * sizeof(int), cudaMemcpyHostToDevice));
-  NMFA_CUDA_TRY(cudaMalloc(&ds->d_ready, mb * sizeof(unsigned)));
+  // Static k-slice order per block: a slice becomes ready when the last tile
+  // covering it (position in its owner pair's list) finishes, so order slices
+  // by that position (ties by index).  Deterministic: depends only on the plan.
+  const int kbn = ds->kblocks;
+  std::vector<int> avail((size_t)mb * kbn, 0);
+  std::vector<unsigned> kneed((size_t)mb * kbn, 0);
+  for (int q = 0; q < pairs; ++q)
+    for (int j = off[q]; j < off[q + 1]; ++j) {
+      const DenseTile& t = tiles[j];
+      for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb) {
+        const int lo_s = std::max(t.n0, kb * 128), hi_s = std::min(t.n0 + t.nlen, kb * 128 + 128);
+        kneed[(size_t)t.m_blk * kbn + kb] += 2u * (unsigned)(hi_s - lo_s);
+        avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
+      }
+    }
+  std::vector<int> korder((size_t)mb * kbn);
+  for (long long m = 0; m < mb; ++m) {
+    int* o = &korder[(size_t)m * kbn];
+    std::iota(o, o + kbn, 0);
+    std::stable_sort(o, o + kbn, [&](int x, int y) {
+      return avail[(size_t)m * kbn + x] < avail[(size_t)m * kbn + y];
+    });
+  }
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int)));
+  NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int),
+                           cudaMemcpyHostToDevice));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_kneed, kneed.size() * sizeof(unsigned)));
+  NMFA_CUDA_TRY(cudaMemcpy(ds->d_kneed, kneed.data(), kneed.size() * sizeof(unsigned),
+                           cudaMemcpyHostToDevice));
+  NMFA_CUDA_TRY(cudaMalloc(&ds->d_ready, kneed.size() * sizeof(unsigned)));
 
   int err;
   for (int b = 0; b < 2; ++b)
@@ -589,11 +631,12 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   }
   *energy_done = energy && dense_energy_exact(p);
   if (*energy_done) NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
-  NMFA_CUDA_TRY(cudaMemsetAsync(ds->d_ready, 0, sizeof(unsigned) * ds->n_mblk, st));
+  NMFA_CUDA_TRY(cudaMemsetAsync(ds->d_ready, 0, sizeof(unsigned) * ds->n_mblk * ds->kblocks, st));
   DenseStepArgs a{};
   a.tiles = ds->d_tiles;
   a.tile_off = ds->d_tile_off;
-  a.m_tiles = ds->d_m_tiles;
+  a.korder = ds->d_korder;
+  a.kneed = ds->d_kneed;
   a.ready = ds->d_ready;
   a.kblocks = ds->kblocks;
   a.k_last_sub = ds->k_last_sub;
