@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #include "common.cuh"
@@ -163,6 +164,14 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -227,20 +236,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       for (int ph = 0; ph < n_phases; ++ph) {
         const int t = a.t_begin + ph;
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
+        int known_m = -1, known = 0;  // leading k-order entries of block known_m ready this sweep
         for (int j = j0; j < j1; ++j) {
           const DenseTile tl = a.tiles[j];
+          if (tl.m_blk != known_m) {
+            known_m = tl.m_blk;
+            known = ph > 0 ? 0 : a.kblocks;
+          }
           const int half = tl.nlen >> 1;
           const int arow = tl.m_blk * 256 + (int)cta * 128;
           const int brow = tl.n0 + (int)cta * half;
           const int* kord = a.korder + tl.m_blk * a.kblocks;
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
             const int kb = kord[ki];
-            if (ph > 0) {  // slice kb of block m for sweep t was written by sweep t-1
-              const int q = tl.m_blk * a.kblocks + kb;
-              const unsigned need = (unsigned)ph * a.kneed[q];
-              if (ld_acquire_gpu(a.ready + q) < need) {
-                while (ld_acquire_gpu(a.ready + q) < need) __nanosleep(20);
+            if (ki >= known) {
+              // slices of block m for sweep t were written by sweep t-1: poll the next
+              // (up to) 8 entries of the k order with independent relaxed loads
+              const int qb = tl.m_blk * a.kblocks;
+              while (known <= ki) {
+                unsigned v[8];
+                const int cnt = min(8, a.kblocks - known);
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                  if (x < cnt) v[x] = ld_relaxed_gpu(a.ready + qb + kord[known + x]);
+                int adv = 0;
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                  if (x < cnt && adv == x && v[x] >= (unsigned)ph * a.kneed[qb + kord[known + x]]) ++adv;
+                known += adv;
+                if (known <= ki) __nanosleep(20);
               }
+              fence_acq_rel_gpu();
               fence_proxy_async_global();
             }
             const int s = it % kDStages;
@@ -360,10 +386,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
             float acc[16], ms[16], lo[16];
             tmem_ld16(tacc + 16 * c, acc);
+#ifdef NMFA_DBG_NOEPI
+            tmem_wait_ld();
+            if (acc[0] == 12345.f) a.lo[0] = 1;
+            continue;
+#endif
+#ifndef NMFA_DBG_NOMEM
             unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), ms);
             unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off + 128), ms + 8);
             unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off), lo);
             unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off + 128), lo + 8);
+#else
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) { ms[cc] = 0.01f * cc; lo[cc] = 0.f; }
+#endif
 #pragma unroll
             for (int cc = 0; cc < 16; ++cc) ms[cc] += lo[cc];
             tmem_wait_ld();
@@ -374,10 +410,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
             uint4 hv[2], lv[2];
             split_half16(ms, hv, lv, last);
+#ifndef NMFA_DBG_NOMEM
             *reinterpret_cast<uint4*>(a_next + off) = hv[0];
             *reinterpret_cast<uint4*>(a_next + off + 128) = hv[1];
             *reinterpret_cast<uint4*>(a.lo + off) = lv[0];
             *reinterpret_cast<uint4*>(a.lo + off + 128) = lv[1];
+#else
+            if (hv[0].x == 0x12345u && lv[1].y == 7u) a.lo[0] = 1;
+#endif
             if (extra) {
               if (a.s_hist) {
                 float* hrow = a.s_hist + ((long long)r * a.t_f + t) * a.n + i0;
@@ -535,29 +575,40 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(cudaMemset(ds->a_img[0], 0, img_bytes));
   NMFA_CUDA_TRY(cudaMemset(ds->a_img[1], 0, img_bytes));
 
-  // balanced static schedule over (replica block, 16-spin unit)
+  // Static schedule.  A tile is (replica block of 256, w x 16 spins); per
+  // k-slice of 128 it costs max(MMA = 64 w, TMA = 563 + 22.6 w) cycles
+  // (profiles/r01/tma_bench2.log: ~100 cycles per box + ~11.3 cycles/KB, one
+  // 32 KB A box + one w*2 KB B box per CTA).  Pick the width minimising the
+  // makespan ceil(tiles / pairs) * cost(w); then give every pair a contiguous
+  // run of whole tiles (counts differ by at most one), so no pair gets a narrow,
+  // TMA-bound remainder tile.
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-  const long long upm = ds->np / 16, mb = ds->Rp / 256, U = upm * mb;
-  const int pairs = (int)std::min<long long>(sms / 2, U);
+  const long long upm = ds->np / 16, mb = ds->Rp / 256;
+  int best_w = 16;
+  double best_cost = 1e300;
+  for (int w = 1; w <= 16; ++w) {
+    const long long tpm = (upm + w - 1) / w, T = tpm * mb;
+    const long long pairs_used = std::min<long long>(sms / 2, T);
+    const double per_slice = std::max(64.0 * w, 563.0 + 22.6 * w);
+    const double makespan = (double)((T + pairs_used - 1) / pairs_used) * per_slice;
+    if (makespan < best_cost - 1e-9) {
+      best_cost = makespan;
+      best_w = w;
+    }
+  }
+  const long long tpm = (upm + best_w - 1) / best_w, T = tpm * mb;
+  const int pairs = (int)std::min<long long>(sms / 2, T);
   ds->pairs = pairs;
   std::vector<DenseTile> tiles;
-  std::vector<int> off(pairs + 1, 0);
-  for (int q = 0; q < pairs; ++q) {
-    long long u = U * q / pairs;
-    const long long u1 = U * (q + 1) / pairs;
-    while (u < u1) {
-      const long long m = u / upm;
-      const long long seg_end = std::min(u1, (m + 1) * upm);
-      // full 256-spin tiles (one 32 KB B box per CTA and stage) + one remainder tile
-      for (long long a0 = u; a0 < seg_end; a0 += 16) {
-        const long long a1 = std::min(seg_end, a0 + 16);
-        tiles.push_back({(int)m, (int)((a0 - m * upm) * 16), (int)((a1 - a0) * 16), 0});
-      }
-      u = seg_end;
+  tiles.reserve(T);
+  for (long long m = 0; m < mb; ++m)
+    for (long long k = 0; k < tpm; ++k) {  // balanced widths within the block
+      const long long a0 = upm * k / tpm, a1 = upm * (k + 1) / tpm;
+      tiles.push_back({(int)m, (int)(a0 * 16), (int)((a1 - a0) * 16), 0});
     }
-    off[q + 1] = (int)tiles.size();
-  }
+  std::vector<int> off(pairs + 1, 0);
+  for (int q = 0; q <= pairs; ++q) off[q] = (int)(T * q / pairs);
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_tiles, tiles.size() * sizeof(DenseTile)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_tiles, tiles.data(), tiles.size() * sizeof(DenseTile),
                            cudaMemcpyHostToDevice));
@@ -581,12 +632,14 @@ int dense_plan_alloc(nmfa_plan* pl) {
       }
     }
   std::vector<int> korder((size_t)mb * kbn);
+  static const bool natural = getenv("NMFA_KORDER_NATURAL") != nullptr;  // A/B experiments
   for (long long m = 0; m < mb; ++m) {
     int* o = &korder[(size_t)m * kbn];
     std::iota(o, o + kbn, 0);
-    std::stable_sort(o, o + kbn, [&](int x, int y) {
-      return avail[(size_t)m * kbn + x] < avail[(size_t)m * kbn + y];
-    });
+    if (!natural)
+      std::stable_sort(o, o + kbn, [&](int x, int y) {
+        return avail[(size_t)m * kbn + x] < avail[(size_t)m * kbn + y];
+      });
   }
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int),
