@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <numeric>
 
@@ -100,6 +101,7 @@ struct DenseStepArgs {
   double* energy;          // energy pass: E[r] accumulator (zeroed)
   const double* h;         // raw fields (energy pass)
   double half_scale;       // 0.5 * j_scale (energy pass)
+  unsigned long long* trace;  // debug timeline (NMFA_TRACE), CTA 0 only
 };
 
 // ---------------------------------------------------------------------------
@@ -247,6 +249,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           const int arow = tl.m_blk * 256 + (int)cta * 128;
           const int brow = tl.n0 + (int)cta * half;
           const int* kord = a.korder + tl.m_blk * a.kblocks;
+          const int jglob = ph * (j1 - j0) + (j - j0);
+          if (a.trace && blockIdx.x == 0 && jglob < 512) a.trace[jglob * 8 + 0] = clock64();
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
             const int kb = kord[ki];
             if (ki >= known) {
@@ -269,6 +273,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               fence_acq_rel_gpu();
               fence_proxy_async_global();
             }
+            if (ki == a.kblocks - 1 && a.trace && blockIdx.x == 0 && jglob < 512)
+              a.trace[jglob * 8 + 1] = clock64();  // producer reached the last slice
             const int s = it % kDStages;
             mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
             const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
@@ -301,6 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           const DenseTile tl = a.tiles[j];
           const int slot = jj & 1, use = jj >> 1;
           mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
+          if (a.trace && jj < 512) a.trace[jj * 8 + 2] = clock64();
           tc_fence_after();
           const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
           const uint32_t d = tbase + (uint32_t)slot * kAccCols;
@@ -320,6 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             commit_pair_mc(&empty_bar[s]);
           }
           commit_pair_mc(&tfull_bar[slot]);
+          if (a.trace && jj < 512) a.trace[jj * 8 + 3] = clock64();
         }
       }
     }
@@ -353,24 +361,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
         const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
         mbar_wait(&tfull_bar[slot], use & 1);
+        if (a.trace && blockIdx.x == 0 && e == 0 && lane == 0 && jj < 512) a.trace[jj * 8 + 4] = clock64();
         tc_fence_after();
         const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
-        const int nch = tl.nlen >> 4;
+        // this warp's columns: a contiguous, 8-aligned quarter of the tile (balanced to 8 spins)
+        const int n8 = tl.nlen >> 3;
+        const int c_lo = (n8 * hpart / 4) * 8, c_hi = (n8 * (hpart + 1) / 4) * 8;
+        auto img_off = [&](int i) {
+          return (long long)(i >> 7) * a.Rp * 256 + row_off + ((i & 127) >> 3) * 128;
+        };
         if (energy_phase) {
           // a_cur holds the +-1 configuration written by the last sweep
           double e_pair = 0.0, e_field = 0.0;
-          for (int c = hpart; c < nch; c += kStep) {
-            const int i0 = tl.n0 + 16 * c;
-            float acc[16];
-            tmem_ld16(tacc + 16 * c, acc);
-            const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
-            float cs[16];
-            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), cs);
-            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off + 128), cs + 8);
+          for (int c = c_lo; c < c_hi; c += 8) {
+            const int i0 = tl.n0 + c;
+            float acc[8], cs[8];
+            tmem_ld8(tacc + c, acc);
+            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + img_off(i0)), cs);
             tmem_wait_ld();
-            const int nvalid = valid ? min(16, a.n - i0) : 0;
+            const int nvalid = valid ? min(8, a.n - i0) : 0;
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
+            for (int cc = 0; cc < 8; ++cc) {
               if (cc < nvalid) {
                 e_pair += (double)(cs[cc] * acc[cc]);        // c_i (J c)_i, exact integers
                 const double hv = __ldg(a.h + i0 + cc);
@@ -381,73 +392,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
         } else {
           const bool extra = valid && (a.s_hist != nullptr || last);
-          for (int c = hpart; c < nch; c += kStep) {
-            const int i0 = tl.n0 + 16 * c;
-            const long long off = (long long)(i0 >> 7) * a.Rp * 256 + row_off + ((i0 & 127) >> 3) * 128;
-            float acc[16], ms[16], lo[16];
-            tmem_ld16(tacc + 16 * c, acc);
-#ifdef NMFA_DBG_NOEPI
-            tmem_wait_ld();
-            if (acc[0] == 12345.f) a.lo[0] = 1;
-            continue;
-#endif
-#ifndef NMFA_DBG_NOMEM
-            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), ms);
-            unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off + 128), ms + 8);
-            unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off), lo);
-            unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off + 128), lo + 8);
-#else
+          auto do_chunk = [&](auto wtag, int c) {
+            constexpr int W = decltype(wtag)::value;
+            const int i0 = tl.n0 + c;
+            float acc[W], ms[W], lo[W];
+            if constexpr (W == 16) tmem_ld16(tacc + c, acc);
+            else tmem_ld8(tacc + c, acc);
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc) { ms[cc] = 0.01f * cc; lo[cc] = 0.f; }
-#endif
+            for (int h = 0; h < W / 8; ++h) {
+              const long long off = img_off(i0 + 8 * h);
+              unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), ms + 8 * h);
+              unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off), lo + 8 * h);
+            }
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc) ms[cc] += lo[cc];
+            for (int cc = 0; cc < W; ++cc) ms[cc] += lo[cc];
             tmem_wait_ld();
-            const int nvalid = valid ? min(16, a.n - i0) : 0;
+            const int nvalid = valid ? min(W, a.n - i0) : 0;
             const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + t) * a.n + i0 : nullptr;
-            update16<kInjected>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
-                                (uint32_t)(i0 / 4), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+            update_chunk<kInjected, W>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
+                                       (uint32_t)(i0 / 4), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
-            uint4 hv[2], lv[2];
-            split_half16(ms, hv, lv, last);
-#ifndef NMFA_DBG_NOMEM
-            *reinterpret_cast<uint4*>(a_next + off) = hv[0];
-            *reinterpret_cast<uint4*>(a_next + off + 128) = hv[1];
-            *reinterpret_cast<uint4*>(a.lo + off) = lv[0];
-            *reinterpret_cast<uint4*>(a.lo + off + 128) = lv[1];
-#else
-            if (hv[0].x == 0x12345u && lv[1].y == 7u) a.lo[0] = 1;
-#endif
+#pragma unroll
+            for (int h = 0; h < W / 8; ++h) {
+              const long long off = img_off(i0 + 8 * h);
+              uint4 hv, lv;
+              split_half8(ms + 8 * h, hv, lv, last);
+              *reinterpret_cast<uint4*>(a_next + off) = hv;
+              *reinterpret_cast<uint4*>(a.lo + off) = lv;
+            }
             if (extra) {
               if (a.s_hist) {
                 float* hrow = a.s_hist + ((long long)r * a.t_f + t) * a.n + i0;
 #pragma unroll
-                for (int cc = 0; cc < 16; ++cc)
+                for (int cc = 0; cc < W; ++cc)
                   if (cc < nvalid) hrow[cc] = ms[cc];
               }
               if (last) {
+                int8_t* crow = a.cfg + r * a.n + i0;
 #pragma unroll
-                for (int cc = 0; cc < 16; ++cc) {
-                  if (cc < nvalid) {
-                    a.cfg[r * a.n + i0 + cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181
-                    if (a.s_out) a.s_out[r * a.n + i0 + cc] = ms[cc];
-                  }
+                for (int cc = 0; cc < W; ++cc)  // sign_round: s < 0 -> -1 else +1 (problem.py:181)
+                  if (cc < nvalid) crow[cc] = ms[cc] < 0.f ? (int8_t)-1 : (int8_t)1;
+                if (a.s_out) {
+#pragma unroll
+                  for (int cc = 0; cc < W; ++cc)
+                    if (cc < nvalid) a.s_out[r * a.n + i0 + cc] = ms[cc];
                 }
               }
             }
-          }
+          };
+          int c = c_lo;
+          for (; c + 16 <= c_hi; c += 16) do_chunk(std::integral_constant<int, 16>{}, c);
+          if (c < c_hi) do_chunk(std::integral_constant<int, 8>{}, c);
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
-        // publish this CTA's rows of the tile for the next sweep of block m
-        asm volatile("bar.sync 1, %0;" ::"n"(kDEpiWarps * 32) : "memory");
-        if (e == 0 && lane == 0) {
-          __threadfence();
-          fence_proxy_async_global();
-          for (int kb = tl.n0 >> 7; kb <= (tl.n0 + tl.nlen - 1) >> 7; ++kb) {
-            const int lo_s = max(tl.n0, kb * 128), hi_s = min(tl.n0 + tl.nlen, kb * 128 + 128);
-            atomicAdd(a.ready + tl.m_blk * a.kblocks + kb, (unsigned)(hi_s - lo_s));
+        if (lane == 0) {
+          mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
+          if (!energy_phase && c_hi > c_lo) {
+            // publish this warp's rows x columns for the next sweep (counted in spin-quarters)
+            __threadfence();
+            fence_proxy_async_global();
+            const int s_lo = tl.n0 + c_lo, s_hi = tl.n0 + c_hi;
+            for (int kb = s_lo >> 7; kb <= (s_hi - 1) >> 7; ++kb)
+              atomicAdd(a.ready + tl.m_blk * a.kblocks + kb,
+                        (unsigned)(min(s_hi, kb * 128 + 128) - max(s_lo, kb * 128)));
           }
         }
       }
@@ -627,7 +635,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
       const DenseTile& t = tiles[j];
       for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb) {
         const int lo_s = std::max(t.n0, kb * 128), hi_s = std::min(t.n0 + t.nlen, kb * 128 + 128);
-        kneed[(size_t)t.m_blk * kbn + kb] += 2u * (unsigned)(hi_s - lo_s);
+        kneed[(size_t)t.m_blk * kbn + kb] += 8u * (unsigned)(hi_s - lo_s);  // 2 CTAs x 4 quarters
         avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
       }
     }
@@ -730,10 +738,28 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   attr[0].val.cooperative = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
+  static const char* trace_path = getenv("NMFA_TRACE");
+  static unsigned long long* trace = nullptr;
+  if (trace_path) {
+    if (!trace) cudaMallocManaged(&trace, 512 * 8 * 8);
+    cudaMemset(trace, 0, 512 * 8 * 8);
+    a.trace = trace;
+  }
   auto kern = noise ? dense_anneal_kernel<true> : dense_anneal_kernel<false>;
   NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1],
                                    ds->tmB[2], ds->tmB[3], ds->tmB[4], a));
   add_launches(2);
+  if (trace_path) {
+    cudaStreamSynchronize(st);
+    FILE* f = fopen(trace_path, "w");
+    if (f) {
+      for (int j = 0; j < 512; ++j) {
+        for (int k = 0; k < 6; ++k) fprintf(f, "%llu ", trace[j * 8 + k]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   return NMFA_OK;
 }
 

@@ -111,33 +111,41 @@ __device__ __forceinline__ void normal4(const PhiloxKey& K, uint32_t q, uint32_t
   box_muller(w.z, w.w, z[2], z[3]);
 }
 
-// The fused update of 16 consecutive spins i0..i0+15 of one replica.
-//   invn4 / hn4 point at the padded per-spin constants for i0 (16-aligned).
+// The fused update of W (8 or 16) consecutive spins i0..i0+W-1 of one replica.
+//   invn4 / hn4 point at the padded per-spin constants for i0 (4-aligned).
 //   kInjected: z comes from `nz` (pre-scaled, may be unaligned, indices < n_valid)
-//   else in-kernel Philox noise scaled by sigma.
-template <bool kInjected>
-__device__ __forceinline__ void update16(const float acc[16], float ms[16], const float4* invn4,
-                                         const float4* hn4, const float* nz, int n_valid,
-                                         const PhiloxKey& K, uint32_t q0, uint32_t t,
-                                         float sigma, float inv_t, float alpha, float oma) {
-  float z[16];
+//   else in-kernel Philox noise scaled by sigma (q0 = i0 / 4).
+template <bool kInjected, int W>
+__device__ __forceinline__ void update_chunk(const float* acc, float* ms, const float4* invn4,
+                                             const float4* hn4, const float* nz, int n_valid,
+                                             const PhiloxKey& K, uint32_t q0, uint32_t t,
+                                             float sigma, float inv_t, float alpha, float oma) {
+  float z[W];
   if (kInjected) {
 #pragma unroll
-    for (int c = 0; c < 16; ++c) z[c] = c < n_valid ? nz[c] : 0.f;
+    for (int c = 0; c < W; ++c) z[c] = c < n_valid ? nz[c] : 0.f;
   } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) normal4(K, q0 + q, t, &z[4 * q]);
+    for (int q = 0; q < W / 4; ++q) normal4(K, q0 + q, t, &z[4 * q]);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) z[c] *= sigma;
+    for (int c = 0; c < W; ++c) z[c] *= sigma;
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < W / 4; ++q) {
     const float4 iv = __ldg(invn4 + q), hv = __ldg(hn4 + q);
     ms[4 * q + 0] = nmfa_update(acc[4 * q + 0], iv.x, hv.x, z[4 * q + 0], inv_t, alpha, oma, ms[4 * q + 0]);
     ms[4 * q + 1] = nmfa_update(acc[4 * q + 1], iv.y, hv.y, z[4 * q + 1], inv_t, alpha, oma, ms[4 * q + 1]);
     ms[4 * q + 2] = nmfa_update(acc[4 * q + 2], iv.z, hv.z, z[4 * q + 2], inv_t, alpha, oma, ms[4 * q + 2]);
     ms[4 * q + 3] = nmfa_update(acc[4 * q + 3], iv.w, hv.w, z[4 * q + 3], inv_t, alpha, oma, ms[4 * q + 3]);
   }
+}
+
+template <bool kInjected>
+__device__ __forceinline__ void update16(const float acc[16], float ms[16], const float4* invn4,
+                                         const float4* hn4, const float* nz, int n_valid,
+                                         const PhiloxKey& K, uint32_t q0, uint32_t t,
+                                         float sigma, float inv_t, float alpha, float oma) {
+  update_chunk<kInjected, 16>(acc, ms, invn4, hn4, nz, n_valid, K, q0, t, sigma, inv_t, alpha, oma);
 }
 
 // ---------------------------------------------------------------------------
@@ -268,6 +276,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float v[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -301,6 +320,26 @@ __device__ __forceinline__ void unpack_half8(const uint4 v, float f[8]) {
     f[2 * k] = t.x;
     f[2 * k + 1] = t.y;
   }
+}
+
+// s -> hi = fp16(s), lo = fp16(s - hi) for 8 values (or hi = sign(s) when `sign`)
+__device__ __forceinline__ void split_half8(const float s[8], uint4& hi, uint4& lo, bool sign) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float a = s[2 * k], b = s[2 * k + 1];
+    if (sign) {
+      a = a < 0.f ? -1.f : 1.f;
+      b = b < 0.f ? -1.f : 1.f;
+    }
+    const __half2 hh = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[k] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 // s -> hi = fp16(s), lo = fp16(s - hi)  (or hi = sign(s), lo = 0 when `sign`)

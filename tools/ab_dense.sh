@@ -3,5 +3,4 @@ run() { NMFA_NVCC_DEFS="$2" python -m paper_1806_08422_b200.build --force > /dev
 run full ""
 run noepi "-DNMFA_DBG_NOEPI"
 run nomem "-DNMFA_DBG_NOMEM"
-run full ""
 python -m paper_1806_08422_b200.build --force > /dev/null 2>&1

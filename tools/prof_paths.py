@@ -9,12 +9,13 @@ if which == "small":
 elif which == "sparse":
     p, R, t_f = nb.gen_dense_maxcut(2000, 0.01, 7), 4096, 8
 else:
-    p, R, t_f = nb.gen_sk(2000, 7), 8192, 3
+    p, R, t_f = nb.gen_sk(2000, 7), 8192, int(os.environ.get("PROF_TF", "3"))
 params = nb.NmfaParams(t_f=t_f, seed=0)
 plan = nb.Plan(p, R, params.schedule.temperatures(t_f), params.alpha, params.sigma)
 cfg = torch.empty((R, p.n), dtype=torch.int8, device="cuda")
 en = torch.empty(R, dtype=torch.float64, device="cuda")
+use_e = os.environ.get("PROF_NO_ENERGY") is None
 for k in range(2):
-    plan.run(k, 0, config=cfg, energy=en)
+    plan.run(k, 0, config=cfg, energy=en if use_e else None)
 torch.cuda.synchronize()
 print(which, "ok", en.min().item())

@@ -20,7 +20,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <int CS>
+template <int CS, int MODE>
 __global__ void __launch_bounds__(64, 1) tma_bench(const __grid_constant__ CUtensorMap tm, int iters,
                                                    long long lines_total, int box_lines) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(64, 1) tma_bench(const __grid_constant__ CUten
   const uint32_t rank = CS > 1 ? cluster_rank() : 0;
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CS); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE == 1 ? 1 : CS); }
     fence_mbar_init();
   }
   if (CS > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;");
@@ -41,23 +41,31 @@ __global__ void __launch_bounds__(64, 1) tma_bench(const __grid_constant__ CUten
       mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], kTile);
       long long line = ((cl * 7919 + it) * 256) % (lines_total - 256);
-      if (CS == 1) {
+      if (CS == 1 || MODE == 1) {   // MODE 1: unicast in a cluster (protocol cost only)
         for (int o = 0; o < kTile / 128; o += box_lines)
         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                      ::"r"(smem_u32(smem + s * kTile + o * 128)), "l"(&tm), "r"(0), "r"((int)line + o), "r"(smem_u32(&full[s])) : "memory");
+      } else if (MODE == 2) {       // MODE 2: rank 0 multicasts the whole stage
+        if (rank == 0)
+          for (int o = 0; o < kTile / 128; o += box_lines)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;"
+                         ::"r"(smem_u32(smem + s * kTile + o * 128)), "l"(&tm), "r"(0), "r"((int)(line + o)),
+                           "r"(smem_u32(&full[s])), "h"((uint16_t)((1 << CS) - 1)) : "memory");
       } else {
-        // each CTA loads 1/CS of the tile and multicasts it to every CTA of the cluster
-        const int part = 128 / CS;
-        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;"
-                     ::"r"(smem_u32(smem + s * kTile + rank * part * 128)), "l"(&tm), "r"(0), "r"((int)(line + rank * part)),
-                       "r"(smem_u32(&full[s])), "h"((uint16_t)((1 << CS) - 1)) : "memory");
+        // each CTA loads 1/CS of the stage (box_lines each) and multicasts it to every CTA
+        const int part = (kTile / 128) / CS;
+        for (int o = 0; o < part; o += box_lines)
+          asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;"
+                       ::"r"(smem_u32(smem + s * kTile + (rank * part + o) * 128)), "l"(&tm), "r"(0),
+                         "r"((int)(line + rank * part + o)), "r"(smem_u32(&full[s])),
+                         "h"((uint16_t)((1 << CS) - 1)) : "memory");
       }
     }
   } else if (warp == 1 && lane == 0) {
     for (int it = 0; it < iters; ++it) {
       const int s = it % kStages;
       mbar_wait(&full[s], (it / kStages) & 1);
-      if (CS == 1) mbar_arrive(&empty[s]);
+      if (CS == 1 || MODE == 1) mbar_arrive(&empty[s]);
       else {
         for (int r = 0; r < CS; ++r) {
           uint32_t a;
@@ -70,10 +78,10 @@ __global__ void __launch_bounds__(64, 1) tma_bench(const __grid_constant__ CUten
   if (CS > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;");
 }
 
-template <int CS>
+template <int CS, int MODE = 0>
 void run(const CUtensorMap& tm, long long lines, const char* name, int box_lines = 128, int grid = 148) {
   const int iters = 4000;
-  auto k = tma_bench<CS>;
+  auto k = tma_bench<CS, MODE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid / CS * CS);
@@ -105,17 +113,17 @@ int main() {
   void* buf;
   cudaMalloc(&buf, bytes);
   cudaMemset(buf, 1, bytes);
-  for (int box : {8, 32, 64, 128, 256}) {
-    CUtensorMap tm;
-    cuuint64_t dims[2] = {64, (cuuint64_t)lines};
-    cuuint64_t strides[1] = {128};
-    cuuint32_t boxd[2] = {64, (cuuint32_t)box}, estr[2] = {1, 1};
-    encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, buf, dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    char name[64];
-    snprintf(name, 64, "unicast box=%d lines", box);
-    run<1>(tm, lines, name, box, 148);
-    if (box == 128) { run<1>(tm, lines, name, box, 74); run<1>(tm, lines, name, box, 37); }
-  }
+  CUtensorMap tm128, tm256;
+  cuuint64_t dims[2] = {64, (cuuint64_t)lines};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t b128[2] = {64, 128}, b256[2] = {64, 256}, estr[2] = {1, 1};
+  encode(&tm128, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, buf, dims, strides, b128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  encode(&tm256, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, buf, dims, strides, b256, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  run<1, 0>(tm256, lines, "unicast box=256", 256, 148);
+  run<2, 1>(tm256, lines, "cluster2 unicast box=256", 256, 148);
+  run<2, 2>(tm256, lines, "cluster2 rank0-multicast 256", 256, 148);
+  run<2, 0>(tm128, lines, "cluster2 split-multicast 128", 128, 148);
   return 0;
 }

@@ -1,0 +1,5 @@
+#!/bin/bash
+NMFA_TRACE=gpurun_out/trace_full.txt timeout 100 python tools/prof_dense.py 40 > /dev/null 2>&1
+NMFA_NVCC_DEFS="-DNMFA_DBG_NOEPI" python -m paper_1806_08422_b200.build --force > /dev/null 2>&1
+NMFA_TRACE=gpurun_out/trace_noepi.txt timeout 100 python tools/prof_dense.py 40 > /dev/null 2>&1
+python -m paper_1806_08422_b200.build --force > /dev/null 2>&1
