@@ -122,11 +122,11 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
-                                           uint32_t mbar_cluster) {
+                                           uint32_t mbar_cluster, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(mbar_cluster)
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(mbar_cluster), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void mbar_remote_arrive(uint32_t mbar_cluster) {
@@ -166,6 +166,32 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// L2 residency: operand images and J are re-read by every pair of a replica
+// block (TMA, evict_last); the lo residual is touched once per sweep per element
+// (evict_first) so it does not push the operands out of L2.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_hint(const void* ptr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -235,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int it = 0;
+      const uint64_t pol_keep = policy_evict_last();
       for (int ph = 0; ph < n_phases; ++ph) {
         const int t = a.t_begin + ph;
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
@@ -281,7 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             if (cta == 0)
               mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
             uint8_t* st = smem + (size_t)s * kDStageBytes;
-            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb);
+            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb, pol_keep);
             int off = 0;  // rows
 #pragma unroll
             for (int b = 4; b >= 0; --b) {
@@ -290,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
                 const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
                                       : b == 1 ? &tmB32 : &tmB16;
                 tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
-                           (kb * a.np + brow + off) * 2, fb);
+                           (kb * a.np + brow + off) * 2, fb, pol_keep);
                 off += rows;
               }
             }
@@ -307,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           const DenseTile tl = a.tiles[j];
           const int slot = jj & 1, use = jj >> 1;
           mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
-          if (a.trace && jj < 512) a.trace[jj * 8 + 2] = clock64();
+          if (a.trace && blockIdx.x == 0 && jj < 512) a.trace[jj * 8 + 2] = clock64();
           tc_fence_after();
           const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
           const uint32_t d = tbase + (uint32_t)slot * kAccCols;
@@ -327,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             commit_pair_mc(&empty_bar[s]);
           }
           commit_pair_mc(&tfull_bar[slot]);
-          if (a.trace && jj < 512) a.trace[jj * 8 + 3] = clock64();
+          if (a.trace && blockIdx.x == 0 && jj < 512) a.trace[jj * 8 + 3] = clock64();
         }
       }
     }
@@ -344,6 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
     const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
     const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
     int jj = 0;
     for (int ph = 0; ph < n_phases; ++ph) {
       const int t = a.t_begin + ph;
@@ -398,11 +426,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             float acc[W], ms[W], lo[W];
             if constexpr (W == 16) tmem_ld16(tacc + c, acc);
             else tmem_ld8(tacc + c, acc);
+#ifdef NMFA_DBG_NOEPI
+            tmem_wait_ld();
+            if (acc[0] == 12345.f) a.lo[0] = 1;
+            return;
+#endif
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
               const long long off = img_off(i0 + 8 * h);
-              unpack_half8(*reinterpret_cast<const uint4*>(a_cur + off), ms + 8 * h);
-              unpack_half8(*reinterpret_cast<const uint4*>(a.lo + off), lo + 8 * h);
+#ifndef NMFA_DBG_NOMEM
+              unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
+              unpack_half8(ld_hint(a.lo + off, pol_stream), lo + 8 * h);
+#else
+#pragma unroll
+              for (int q = 0; q < 8; ++q) { ms[8 * h + q] = 0.01f * q; lo[8 * h + q] = 0.f; }
+#endif
             }
 #pragma unroll
             for (int cc = 0; cc < W; ++cc) ms[cc] += lo[cc];
@@ -410,15 +448,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             const int nvalid = valid ? min(W, a.n - i0) : 0;
             const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + t) * a.n + i0 : nullptr;
             update_chunk<kInjected, W>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
-                                       (uint32_t)(i0 / 4), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+                                       (uint32_t)(i0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
               const long long off = img_off(i0 + 8 * h);
               uint4 hv, lv;
               split_half8(ms + 8 * h, hv, lv, last);
-              *reinterpret_cast<uint4*>(a_next + off) = hv;
-              *reinterpret_cast<uint4*>(a.lo + off) = lv;
+#ifndef NMFA_DBG_NOMEM
+              st_hint(a_next + off, hv, pol_keep);
+              st_hint(a.lo + off, lv, pol_stream);
+#else
+              if (hv.x == 0x12345u && lv.y == 7u) a.lo[0] = 1;
+#endif
             }
             if (extra) {
               if (a.s_hist) {
@@ -446,6 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 512) atomicMax(&a.trace[jj * 8 + 5], clock64());
         if (lane == 0) {
           mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
           if (!energy_phase && c_hi > c_lo) {

@@ -1,11 +1,11 @@
 // Sparse NMFA step (CSR gather), one launch per step.
 // State layout: S[i][r] fp32, replicas contiguous (Rp = R rounded up to 32),
 // ping-pong between two buffers (synchronous update, SPEC: all mean fields
-// from the incoming S).  One warp owns a quad of spins (4 consecutive i) for
-// 32 consecutive replicas: every CSR entry (j, w) is a warp-uniform broadcast
-// and the gather S[j][r..r+31] is one coalesced 128-byte load.  The quad
+// from the incoming S).  One warp owns a group of 8 consecutive spins for 32
+// consecutive replicas: every CSR entry (j, w) is a warp-uniform broadcast
+// and the gather S[j][r..r+31] is one coalesced 128-byte load.  The group
 // matches the Philox counter granularity, so one Philox call per thread
-// feeds the four spins (common.cuh noise identity).
+// feeds its eight spins (common.cuh noise identity).
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
 #include "common.cuh"
 #include "internal.h"
@@ -37,13 +37,13 @@ __global__ void __launch_bounds__(256) sparse_step_kernel(const SparseStepArgs a
   const long long nrb = a.Rp / 32;
   const long long q = wg / nrb;
   const long long rb = wg - q * nrb;
-  if (4 * q >= a.n) return;
+  if (8 * q >= a.n) return;
   const long long r = rb * 32 + lane;
 
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int qq = 0; qq < 4; ++qq) {
-    const int i = (int)(4 * q) + qq;
+  for (int qq = 0; qq < 8; ++qq) {
+    const int i = (int)(8 * q) + qq;
     if (i < a.n) {
       const int k1 = __ldg(a.ptr + i + 1);
       float s = 0.f;
@@ -53,22 +53,22 @@ __global__ void __launch_bounds__(256) sparse_step_kernel(const SparseStepArgs a
     }
   }
   const bool valid = r < a.R;
-  float z[4];
+  float z[8];
   if (a.noise) {
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      const int i = (int)(4 * q) + qq;
+    for (int qq = 0; qq < 8; ++qq) {
+      const int i = (int)(8 * q) + qq;
       z[qq] = (valid && i < a.n) ? a.noise[((long long)r * a.t_f + a.t) * a.n + i] : 0.f;
     }
   } else {
     const unsigned long long key = a.key_base + (unsigned long long)r;
-    normal4(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t, z);
+    normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t, z);
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) z[qq] *= a.sigma;
+    for (int qq = 0; qq < 8; ++qq) z[qq] *= a.sigma;
   }
 #pragma unroll
-  for (int qq = 0; qq < 4; ++qq) {
-    const int i = (int)(4 * q) + qq;
+  for (int qq = 0; qq < 8; ++qq) {
+    const int i = (int)(8 * q) + qq;
     if (i >= a.n) break;
     const long long o = (long long)i * a.Rp + r;
     const float s = nmfa_update(acc[qq], __ldg(a.invn + i), __ldg(a.hn + i), z[qq], a.inv_t,
@@ -119,7 +119,7 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
-  const long long warps = ((p->n + 3) / 4) * (pl->Rp / 32);
+  const long long warps = ((p->n + 7) / 8) * (pl->Rp / 32);
   const unsigned blocks = (unsigned)((warps + 7) / 8);
   float* cur = pl->d_sa;
   float* nxt = pl->d_sb;

@@ -20,6 +20,14 @@ namespace nmfa {
 // ---------------------------------------------------------------------------
 constexpr float kOneMinus = 0.99999994f;  // largest float below 1
 
+#ifdef NMFA_DBG_NOMUFU  // timing experiment only: MUFU ops replaced by FMAs (wrong values)
+__device__ __forceinline__ float ex2_approx(float x) { return fmaf(x, 0.69f, 1.0f); }
+__device__ __forceinline__ float rcp_approx(float x) { return fmaf(x, -0.5f, 1.5f); }
+__device__ __forceinline__ float sqrt_approx(float x) { return fmaf(x, 0.5f, 0.5f); }
+__device__ __forceinline__ float lg2_approx(float x) { return fmaf(x, 1.44f, -1.0f); }
+#define NMFA_SINCOS(x, s, c) do { s = fmaf(x, 0.9f, 0.1f); c = fmaf(x, -0.4f, 1.0f); } while (0)
+#else
+#define NMFA_SINCOS(x, s, c) __sincosf(x, &s, &c)
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -40,6 +48,7 @@ __device__ __forceinline__ float lg2_approx(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+#endif
 
 // tanh(y) = sign(y) * (1 - 2 / (exp(2|y|) + 1)): two MUFU ops, absolute error
 // ~1e-7, exactly odd.  exp overflow -> inf -> rcp 0 -> 1.
@@ -60,10 +69,11 @@ __device__ __forceinline__ float nmfa_update(float acc, float inv_norm, float h_
 // ---------------------------------------------------------------------------
 // Counter-based noise.  Stream identity (documented in DESIGN.md):
 //   key     = (lo32(seed + r), hi32(seed + r))      r = GLOBAL replica index
-//   counter = (i >> 2, t, 0x4E4D4641 'NMFA', 0)      i = spin, t = 0-based step
-// Philox4x32-10 gives 4 words -> two Box-Muller pairs -> N(0,1) for spins
-// 4q..4q+3.  Every kernel path (small / dense / sparse) and every sharding of
-// replicas over GPUs therefore sees the same noise for (r, t, i).
+//   counter = (i >> 3, t, 0x4E4D4641 'NMFA', 0)      i = spin, t = 0-based step
+// Philox4x32-10 gives 4 words, each word one Box-Muller pair (20-bit radius,
+// 12-bit angle) -> N(0,1) for spins 8q..8q+7.  Every kernel path (small /
+// dense / sparse) and every sharding of replicas over GPUs therefore sees the
+// same noise for (r, t, i).
 // ---------------------------------------------------------------------------
 struct uint4_ { uint32_t x, y, z, w; };
 
@@ -92,29 +102,33 @@ __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32
 
 constexpr uint32_t kNoiseTag = 0x4E4D4641u;
 
-// Box-Muller on two 32-bit words.  u1 = (k + 1/2) 2^-23 in (0, 1) from the top
-// 23 bits (never 0 or 1), u2 = k 2^-23 in [0, 1).  Tail bound |z| <= 5.78.
-__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
-  const float u1 = fmaf((float)(a >> 9), 1.1920928955078125e-07f, 5.9604644775390625e-08f);
-  const float u2 = (float)(b >> 9) * 1.1920928955078125e-07f;
+// Box-Muller on ONE 32-bit word: the top 20 bits give u1 = (k + 1/2) 2^-20 in
+// (0, 1) (never 0 or 1, tail bound |z| <= 5.40), the low 12 bits the angle
+// u2 = k 2^-12 (equispaced angles: E[cos^2] = 1/2, E[cos^4] = 3/8 exactly).
+__device__ __forceinline__ void box_muller(uint32_t w, float& z0, float& z1) {
+  const float u1 = fmaf((float)(w >> 12), 9.5367431640625e-07f, 4.76837158203125e-07f);
+  const float u2 = (float)(w & 0xFFFu) * 2.44140625e-04f;
   const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u1));  // -2 ln u1
   float sn, cs;
-  __sincosf(6.283185307179586f * u2, &sn, &cs);
+  NMFA_SINCOS(6.283185307179586f * u2, sn, cs);
   z0 = r * cs;
   z1 = r * sn;
 }
 
-// Four standard normals for spins 4q..4q+3 of replica key (k0,k1) at step t.
-__device__ __forceinline__ void normal4(const PhiloxKey& K, uint32_t q, uint32_t t, float z[4]) {
-  uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, K);
-  box_muller(w.x, w.y, z[0], z[1]);
-  box_muller(w.z, w.w, z[2], z[3]);
+// Eight standard normals for spins 8q..8q+7 of replica key K at step t:
+// one Philox4x32-10 call, one Box-Muller pair per output word.
+__device__ __forceinline__ void normal8(const PhiloxKey& K, uint32_t q, uint32_t t, float z[8]) {
+  const uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, K);
+  box_muller(w.x, z[0], z[1]);
+  box_muller(w.y, z[2], z[3]);
+  box_muller(w.z, z[4], z[5]);
+  box_muller(w.w, z[6], z[7]);
 }
 
 // The fused update of W (8 or 16) consecutive spins i0..i0+W-1 of one replica.
 //   invn4 / hn4 point at the padded per-spin constants for i0 (4-aligned).
 //   kInjected: z comes from `nz` (pre-scaled, may be unaligned, indices < n_valid)
-//   else in-kernel Philox noise scaled by sigma (q0 = i0 / 4).
+//   else in-kernel Philox noise scaled by sigma (q0 = i0 / 8; i0 8-aligned).
 template <bool kInjected, int W>
 __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const float4* invn4,
                                              const float4* hn4, const float* nz, int n_valid,
@@ -126,7 +140,7 @@ __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const 
     for (int c = 0; c < W; ++c) z[c] = c < n_valid ? nz[c] : 0.f;
   } else {
 #pragma unroll
-    for (int q = 0; q < W / 4; ++q) normal4(K, q0 + q, t, &z[4 * q]);
+    for (int q = 0; q < W / 8; ++q) normal8(K, q0 + q, t, &z[8 * q]);
 #pragma unroll
     for (int c = 0; c < W; ++c) z[c] *= sigma;
   }
