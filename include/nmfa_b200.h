@@ -63,6 +63,18 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* edges_i_host,
                         const double* h_host, int32_t device, nmfa_problem_t** out);
 int nmfa_problem_destroy(nmfa_problem_t* p);
 int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info);
+/* Synthetic Sherrington-Kirkpatrick instance generated ON DEVICE (BASELINE
+ * config 5, SK N = 65,536: the reference cannot build it, problem.py:41-104
+ * would need >150 GB of host arrays).  J_ij = +-1 for every pair i != j from a
+ * counter-based hash: bit (b mod 128) of Philox4x32-10(key = seed, counter =
+ * (b >> 7, a, 0x534B4A31 'SKJ1', 0)) with a = min(i,j), b = max(i,j), set bit
+ * -> +1; h = 0 (same distribution as gen_sk, generators.py:27-35, not the same
+ * stream).  Only rows [row_lo, row_hi) of J are materialised (row sharding:
+ * row_lo a multiple of 128, row_hi a multiple of 128 or n).  Energies come
+ * from the tensor-core energy pass; nmfa_energy is not available. */
+int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                                  int32_t device, nmfa_problem_t** out);
+
 /* Force a kernel path (tests / crossover studies); NMFA_ERR_ARG if the path
  * cannot run this problem (e.g. SMALL with n > 256). */
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path);
@@ -89,6 +101,30 @@ int nmfa_plan_destroy(nmfa_plan_t* plan);
 int nmfa_plan_run(nmfa_plan_t* plan, uint64_t seed, int64_t r0, const float* noise_dev,
                   const float* s0_dev, int8_t* config_dev, double* energy_dev,
                   float* s_final_dev, float* s_hist_dev, double* e_hist_dev, void* stream);
+
+/* Run sweeps [t_begin, t_end) of the plan's schedule (dense path), then, if
+ * energy_pass, the exact tensor-core energy pass into energy_dev (partial over
+ * the device's row shard for a row-sharded problem).  t_begin == 0
+ * (re)initialises the state from s0_dev / zeros.  A row-sharded problem must
+ * run one sweep per call: between calls the host all-gathers every shard's
+ * k-slices of the next operand image (nmfa_plan_image_info).  config_dev, if
+ * not NULL, receives the configuration of this device's spins at the last
+ * sweep (use nmfa_plan_read_config for the all-gathered one). */
+int nmfa_plan_run_sweeps(nmfa_plan_t* plan, uint64_t seed, int64_t r0, int32_t t_begin,
+                         int32_t t_end, int32_t energy_pass, int8_t* config_dev,
+                         double* energy_dev, void* stream);
+
+/* Operand images of a dense plan (the hi part of the replica state, fp16,
+ * tiled): image[p] for sweep parity p.  Spins [128k, 128k+128) of all replicas
+ * occupy bytes [k * slice_bytes, (k+1) * slice_bytes); this device writes
+ * slices [slice_lo, slice_hi). */
+int nmfa_plan_image_info(const nmfa_plan_t* plan, void** image0, void** image1,
+                         int64_t* slice_bytes, int32_t* n_slices, int32_t* slice_lo,
+                         int32_t* slice_hi);
+
+/* +-1 configurations [n_reads][n] from the (all-gathered) sign image that the
+ * last sweep t_f-1 wrote (parity t_f & 1). */
+int nmfa_plan_read_config(const nmfa_plan_t* plan, int8_t* config_dev, void* stream);
 
 /* One-shot convenience over plan_create/plan_run/plan_destroy. */
 int nmfa_anneal(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,

@@ -302,3 +302,42 @@ def moebius_edges(n):
 
 def problem_from_edges(n, ii, jj, w, h=None):
     return Problem(n, np.column_stack([ii, jj, w]), h)
+
+
+# --------------------------------------------------------------------------
+# Twin of the on-device SK generator (nmfa_problem_create_sk_device,
+# include/nmfa_b200.h) -- test infrastructure for config 5 (SK N = 65,536),
+# which the reference itself cannot build (problem.py:41-104).
+# --------------------------------------------------------------------------
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Vectorised Philox4x32-10 (Salmon et al. 2011) on uint32 numpy arrays."""
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint32).copy() for x in (c0, c1, c2, c3))
+    k0 = np.uint32(k0)
+    k1 = np.uint32(k1)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = c0.astype(np.uint64) * M0
+            p1 = c2.astype(np.uint64) * M1
+            n0 = (p1 >> np.uint64(32)).astype(np.uint32) ^ c1 ^ k0
+            n2 = (p0 >> np.uint64(32)).astype(np.uint32) ^ c3 ^ k1
+            c0, c1, c2, c3 = n0, p1.astype(np.uint32), n2, p0.astype(np.uint32)
+            k0 = np.uint32((int(k0) + int(W0)) & 0xFFFFFFFF)
+            k1 = np.uint32((int(k1) + int(W1)) & 0xFFFFFFFF)
+    return c0, c1, c2, c3
+
+
+def sk_device_couplings(n, seed):
+    """Dense +-1 J of the device-generated SK instance (zero diagonal)."""
+    i, j = np.triu_indices(int(n), 1)
+    a = i.astype(np.uint32)
+    b = j.astype(np.uint32)
+    words = philox4x32_10(b >> np.uint32(7), a, np.uint32(0x534B4A31), np.uint32(0),
+                          int(seed) & 0xFFFFFFFF, (int(seed) >> 32) & 0xFFFFFFFF)
+    sel = (b & np.uint32(127)) >> np.uint32(5)
+    w = np.choose(sel.astype(np.int64), words)
+    bit = (w >> (b & np.uint32(31))) & np.uint32(1)
+    J = np.zeros((n, n))
+    J[i, j] = np.where(bit == 1, 1.0, -1.0)
+    return J + J.T

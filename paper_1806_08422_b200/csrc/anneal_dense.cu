@@ -62,6 +62,7 @@ struct DenseTile {
 
 struct DenseState {
   int np = 0, kp = 0, kblocks = 0, k_last_sub = 0, pairs = 0;
+  int slice_lo = 0, slice_hi = 0;  // k-slices of the image this device writes
   long long Rp = 0;
   uint8_t* lo_img = nullptr;
   uint8_t* a_img[2] = {nullptr, nullptr};
@@ -82,7 +83,7 @@ struct DenseStepArgs {
   const unsigned* kneed;   // [m][kblocks] spins a sweep publishes into the slice (both CTAs)
   unsigned* ready;         // [m][kblocks] spins published so far this launch
   int kblocks, k_last_sub;
-  int n, np;
+  int n, brows, row_lo;    // B image rows (row shard of J) and the shard's first spin
   long long R, Rp;
   int t_begin, t_end, t_f;  // sweeps [t_begin, t_end) of t_f; energy pass after t_f-1
   int energy_pass;
@@ -274,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           }
           const int half = tl.nlen >> 1;
           const int arow = tl.m_blk * 256 + (int)cta * 128;
-          const int brow = tl.n0 + (int)cta * half;
+          const int brow = tl.n0 - a.row_lo + (int)cta * half;  // row within this shard of J
           const int* kord = a.korder + tl.m_blk * a.kblocks;
           const int jglob = ph * (j1 - j0) + (j - j0);
           if (a.trace && blockIdx.x == 0 && jglob < 512) a.trace[jglob * 8 + 0] = clock64();
@@ -317,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
                 const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
                                       : b == 1 ? &tmB32 : &tmB16;
                 tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
-                           (kb * a.np + brow + off) * 2, fb, pol_keep);
+                           (kb * a.brows + brow + off) * 2, fb, pol_keep);
                 off += rows;
               }
             }
@@ -365,7 +366,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     // layout, so s = hi + lo carries ~22 bits and the per-sweep working set
     // (2 images + lo + J) is ~104 MB at K2000 / 8192 reads.
     const int e = warp, quarter = e & 3, hpart = e >> 2;  // lane quarter x column part
-    constexpr int kStep = kDEpiWarps / 4;
     const int row = 32 * quarter + lane;
     const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
     const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
@@ -591,6 +591,54 @@ int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jd) {
   p->j_dense_bytes = img.size() * 2;
   NMFA_CUDA_TRY(cudaMalloc(&p->d_j_dense, p->j_dense_bytes));
   NMFA_CUDA_TRY(cudaMemcpy(p->d_j_dense, img.data(), p->j_dense_bytes, cudaMemcpyHostToDevice));
+  p->row_lo = 0;
+  p->row_hi = p->n;
+  p->brows = (int32_t)np;
+  return NMFA_OK;
+}
+
+// J image rows [row_lo, row_lo + brows) of the synthetic SK instance (see
+// nmfa_problem_create_sk_device): one thread per (row, 8 consecutive k).
+__global__ void sk_image_kernel(uint8_t* img, long long n, int brows, long long row_lo, int kp,
+                                unsigned long long seed) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_row = kp / 8;
+  if (e >= (long long)brows * per_row) return;
+  const int lrow = (int)(e / per_row);
+  const int k0 = (int)(e - (long long)lrow * per_row) * 8;
+  const long long i = row_lo + lrow;
+  const PhiloxKey K = philox_schedule((uint32_t)seed, (uint32_t)(seed >> 32));
+  float v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const long long k = k0 + c;
+    v[c] = 0.f;
+    if (i < n && k < n && k != i) {
+      const uint32_t a = (uint32_t)(i < k ? i : k), b = (uint32_t)(i < k ? k : i);
+      const uint4_ w = philox4x32_10(b >> 7, a, 0x534B4A31u, 0u, K);
+      const uint32_t word = ((b & 127u) >> 5) == 0 ? w.x : ((b & 127u) >> 5) == 1 ? w.y
+                          : ((b & 127u) >> 5) == 2 ? w.z : w.w;
+      v[c] = ((word >> (b & 31u)) & 1u) ? 1.f : -1.f;
+    }
+  }
+  const long long off = (long long)(k0 >> 7) * brows * 256 + (lrow >> 3) * 2048 +
+                        ((k0 & 127) >> 3) * 128 + (lrow & 7) * 16;
+  *reinterpret_cast<uint4*>(img + off) =
+      make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+                 pack_half2(v[6], v[7]));
+}
+
+int dense_problem_generate_sk(nmfa_problem* p, uint64_t seed) {
+  const int kp = (int)((p->n + kBK - 1) / kBK * kBK);
+  const size_t bytes = (size_t)kp * p->brows * 2;
+  p->j_dense_bytes = bytes;
+  NMFA_CUDA_TRY(cudaMalloc(&p->d_j_dense, bytes));
+  NMFA_CUDA_TRY(cudaMemset(p->d_j_dense, 0, bytes));
+  const long long tot = (long long)p->brows * (kp / 8);
+  sk_image_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(
+      reinterpret_cast<uint8_t*>(p->d_j_dense), p->n, p->brows, p->row_lo, kp, seed);
+  NMFA_LAUNCH_CHECK();
+  NMFA_CUDA_TRY(cudaDeviceSynchronize());
   return NMFA_OK;
 }
 
@@ -635,7 +683,10 @@ int dense_plan_alloc(nmfa_plan* pl) {
   // TMA-bound remainder tile.
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-  const long long upm = ds->np / 16, mb = ds->Rp / 256;
+  // tiles cover this device's spins [row_lo, row_lo + brows) only
+  ds->slice_lo = (int)(p->row_lo / kBK);
+  ds->slice_hi = (int)((p->row_hi + kBK - 1) / kBK);
+  const long long upm = p->brows / 16, mb = ds->Rp / 256;
   int best_w = 16;
   double best_cost = 1e300;
   for (int w = 1; w <= 16; ++w) {
@@ -656,7 +707,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
   for (long long m = 0; m < mb; ++m)
     for (long long k = 0; k < tpm; ++k) {  // balanced widths within the block
       const long long a0 = upm * k / tpm, a1 = upm * (k + 1) / tpm;
-      tiles.push_back({(int)m, (int)(a0 * 16), (int)((a1 - a0) * 16), 0});
+      tiles.push_back({(int)m, (int)(p->row_lo + a0 * 16), (int)((a1 - a0) * 16), 0});
     }
   std::vector<int> off(pairs + 1, 0);
   for (int q = 0; q <= pairs; ++q) off[q] = (int)(T * q / pairs);
@@ -667,9 +718,11 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(
       cudaMemcpy(ds->d_tile_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
   ds->n_mblk = (int)mb;
-  // Static k-slice order per block: a slice becomes ready when the last tile
-  // covering it (position in its owner pair's list) finishes, so order slices
-  // by that position (ties by index).  Deterministic: depends only on the plan.
+  // K order: natural (k-slice 0 first), so the fp32 accumulation order of a
+  // spin's field does not depend on the schedule or on the row sharding
+  // (results are identical for any number of shards).  An early-ready-first
+  // order was measured: no gain (profiles/r01).  Readiness is counted per
+  // (replica block, k-slice) in spin-quarters; slices of other shards need 0.
   const int kbn = ds->kblocks;
   std::vector<int> avail((size_t)mb * kbn, 0);
   std::vector<unsigned> kneed((size_t)mb * kbn, 0);
@@ -683,15 +736,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
       }
     }
   std::vector<int> korder((size_t)mb * kbn);
-  static const bool natural = getenv("NMFA_KORDER_NATURAL") != nullptr;  // A/B experiments
-  for (long long m = 0; m < mb; ++m) {
-    int* o = &korder[(size_t)m * kbn];
-    std::iota(o, o + kbn, 0);
-    if (!natural)
-      std::stable_sort(o, o + kbn, [&](int x, int y) {
-        return avail[(size_t)m * kbn + x] < avail[(size_t)m * kbn + y];
-      });
-  }
+  for (long long m = 0; m < mb; ++m) std::iota(&korder[(size_t)m * kbn], &korder[(size_t)m * kbn] + kbn, 0);
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int),
                            cudaMemcpyHostToDevice));
@@ -705,7 +750,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
     if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
       return err;
   for (int b = 0; b < 5; ++b)
-    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * ds->np * 2, 16u << b)))
+    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * p->brows * 2, 16u << b)))
       return err;
   NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_anneal_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
@@ -714,27 +759,32 @@ int dense_plan_alloc(nmfa_plan* pl) {
   return NMFA_OK;
 }
 
-int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
-                        const float* s0, int8_t* cfg, float* s_out, float* s_hist,
-                        double* energy, bool* energy_done, cudaStream_t st) {
+// Sweeps [t_begin, t_end) (+ the energy pass) in ONE persistent launch.
+// t_begin == 0 initialises the state from s0 (or zeros).
+int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise, const float* s0,
+                     int8_t* cfg, float* s_out, float* s_hist, double* energy, int t_begin,
+                     int t_end, bool energy_pass, cudaStream_t st) {
   const nmfa_problem* p = pl->p;
   auto* ds = static_cast<DenseState*>(pl->dense);
   if (!ds) {
     set_error("dense plan state missing");
     return NMFA_ERR_STATE;
   }
+  int64_t launches = 1;
   const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
-  if (s0) {
-    const long long tot = (long long)(ds->kp / 8) * ds->Rp;
-    dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
-    NMFA_LAUNCH_CHECK();
-  } else {  // S(0) = 0 (solver.py:200-201)
-    NMFA_CUDA_TRY(cudaMemsetAsync(ds->a_img[0], 0, img_bytes, st));
-    NMFA_CUDA_TRY(cudaMemsetAsync(ds->lo_img, 0, img_bytes, st));
+  if (t_begin == 0) {
+    if (s0) {
+      const long long tot = (long long)(ds->kp / 8) * ds->Rp;
+      dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
+      NMFA_LAUNCH_CHECK();
+      ++launches;
+    } else {  // S(0) = 0 (solver.py:200-201)
+      NMFA_CUDA_TRY(cudaMemsetAsync(ds->a_img[0], 0, img_bytes, st));
+      NMFA_CUDA_TRY(cudaMemsetAsync(ds->lo_img, 0, img_bytes, st));
+    }
   }
-  *energy_done = energy && dense_energy_exact(p);
-  if (*energy_done) NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
+  if (energy_pass) NMFA_CUDA_TRY(cudaMemsetAsync(energy, 0, sizeof(double) * pl->R, st));
   NMFA_CUDA_TRY(cudaMemsetAsync(ds->d_ready, 0, sizeof(unsigned) * ds->n_mblk * ds->kblocks, st));
   DenseStepArgs a{};
   a.tiles = ds->d_tiles;
@@ -745,13 +795,14 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.kblocks = ds->kblocks;
   a.k_last_sub = ds->k_last_sub;
   a.n = (int)p->n;
-  a.np = ds->np;
+  a.brows = p->brows;
+  a.row_lo = (int)p->row_lo;
   a.R = pl->R;
   a.Rp = ds->Rp;
-  a.t_begin = 0;
-  a.t_end = pl->t_f;
+  a.t_begin = t_begin;
+  a.t_end = t_end;
   a.t_f = pl->t_f;
-  a.energy_pass = *energy_done ? 1 : 0;
+  a.energy_pass = energy_pass ? 1 : 0;
   a.alpha = pl->alpha;
   a.oma = pl->oma;
   a.sigma = pl->sigma;
@@ -791,7 +842,7 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   auto kern = noise ? dense_anneal_kernel<true> : dense_anneal_kernel<false>;
   NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1],
                                    ds->tmB[2], ds->tmB[3], ds->tmB[4], a));
-  add_launches(2);
+  add_launches(launches);
   if (trace_path) {
     cudaStreamSynchronize(st);
     FILE* f = fopen(trace_path, "w");
@@ -803,6 +854,64 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
       fclose(f);
     }
   }
+  return NMFA_OK;
+}
+
+bool dense_is_sharded(const nmfa_problem* p) { return p->row_lo != 0 || p->row_hi != p->n; }
+
+int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+                        const float* s0, int8_t* cfg, float* s_out, float* s_hist,
+                        double* energy, bool* energy_done, cudaStream_t st) {
+  if (dense_is_sharded(pl->p)) {
+    set_error("a row-sharded problem runs one sweep per nmfa_plan_run_sweeps call "
+              "with an all-gather of the operand image in between");
+    return NMFA_ERR_STATE;
+  }
+  *energy_done = energy && dense_energy_exact(pl->p);
+  return dense_run_sweeps(pl, key_base, noise, s0, cfg, s_out, s_hist, energy, 0, pl->t_f,
+                          *energy_done, st);
+}
+
+int dense_image_info(const nmfa_plan* pl, void** img0, void** img1, int64_t* slice_bytes,
+                     int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi) {
+  auto* ds = static_cast<DenseState*>(pl->dense);
+  if (!ds) {
+    set_error("not a dense plan");
+    return NMFA_ERR_STATE;
+  }
+  *img0 = ds->a_img[0];
+  *img1 = ds->a_img[1];
+  *slice_bytes = ds->Rp * 256;
+  *n_slices = ds->kblocks;
+  *slice_lo = ds->slice_lo;
+  *slice_hi = ds->slice_hi;
+  return NMFA_OK;
+}
+
+// cfg[r][i] = sign of the fp16 +-1 sign image
+__global__ void read_config_kernel(const uint8_t* img, int8_t* cfg, int n, long long R,
+                                   long long Rp) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * R) return;
+  const long long r = e / n;
+  const int i = (int)(e - r * n);
+  const long long off = (long long)(i >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
+                        (r & 7) * 16 + (i & 7) * 2;
+  const __half h = *reinterpret_cast<const __half*>(img + off);
+  cfg[e] = __half2float(h) < 0.f ? (int8_t)-1 : (int8_t)1;
+}
+
+int dense_read_config(const nmfa_plan* pl, int8_t* cfg, cudaStream_t st) {
+  auto* ds = static_cast<DenseState*>(pl->dense);
+  if (!ds) {
+    set_error("not a dense plan");
+    return NMFA_ERR_STATE;
+  }
+  const long long tot = pl->p->n * pl->R;
+  read_config_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      ds->a_img[pl->t_f & 1], cfg, (int)pl->p->n, pl->R, ds->Rp);
+  NMFA_LAUNCH_CHECK();
+  add_launches(1);
   return NMFA_OK;
 }
 

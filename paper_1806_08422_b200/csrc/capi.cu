@@ -274,6 +274,59 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
   return NMFA_OK;
 }
 
+int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                                  int32_t device, nmfa_problem_t** out) {
+  if (!out) return arg_error("out pointer is NULL");
+  *out = nullptr;
+  if (n < 2) return arg_error("sk generator needs n >= 2, got " + std::to_string(n));
+  if (n > (int64_t)1 << 20) return arg_error("spin count too large for the dense path");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi)
+    return arg_error("row shard must satisfy 0 <= row_lo < row_hi <= n");
+  if (row_lo % 128 != 0 || (row_hi % 128 != 0 && row_hi != n))
+    return arg_error("row shard boundaries must be multiples of 128 (or n)");
+  auto* p = new nmfa_problem();
+  p->device = device;
+  p->n = n;
+  p->n_edges = n * (n - 1) / 2;
+  p->density = 1.0;
+  p->is_dense = true;
+  p->path = NMFA_PATH_DENSE;
+  p->int_weights = true;
+  p->j_exact = true;
+  p->j_scale = 1.0;
+  p->max_row_abs = (double)(n - 1);
+  p->device_generated = true;
+  p->sk_seed = seed;
+  p->h.assign(n, 0.0);
+  p->norm_safe.assign(n, std::sqrt((double)(n - 1)));  // every row holds n-1 couplings of |w| = 1
+  p->row_lo = row_lo;
+  p->row_hi = row_hi;
+  p->brows = (int32_t)((row_hi - row_lo + 15) / 16 * 16);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete p;
+    return arg_error("invalid CUDA device " + std::to_string(device));
+  }
+  int err = NMFA_OK;
+  do {
+    p->np = (int32_t)((n + 15) / 16 * 16);
+    std::vector<float> invn(p->np, 0.f), hn(p->np, 0.f);
+    for (int64_t i = 0; i < n; ++i) invn[i] = (float)(1.0 / p->norm_safe[i]);
+    if ((err = upload(&p->d_invn, invn.data(), invn.size()))) break;
+    if ((err = upload(&p->d_hn, hn.data(), hn.size()))) break;
+    if ((err = upload(&p->d_h, p->h.data(), p->h.size()))) break;
+    err = dense_problem_generate_sk(p, seed);
+  } while (0);
+  cudaSetDevice(prev);
+  if (err) {
+    nmfa_problem_destroy(p);
+    return err;
+  }
+  *out = p;
+  return NMFA_OK;
+}
+
 int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
   if (!p || !info) return arg_error("NULL argument");
   info->n = p->n;
@@ -289,6 +342,8 @@ int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
 
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
   if (!p) return arg_error("NULL problem");
+  if (p->device_generated && path != NMFA_PATH_DENSE)
+    return arg_error("a device-generated problem only runs the dense path");
   if (path == NMFA_PATH_SMALL && !p->d_j_small)
     return arg_error("small path needs n <= 256");
   if (path == NMFA_PATH_DENSE && !p->d_j_dense) {
@@ -425,6 +480,10 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
     default:
       err = launch_sparse_anneal(pl, key_base, noise, s0, cfg, s_out, s_hist, st);
   }
+  if (!err && energy && !energy_done && p->device_generated) {
+    set_error("energies of a device-generated problem need the tensor-core pass");
+    err = NMFA_ERR_STATE;
+  }
   if (!err && energy && !energy_done)
     err = launch_energy(p, cfg, pl->R, energy, pl->d_bits, pl->d_epart, pl->energy_chunks, st);
   if (!err && e_hist) {
@@ -447,6 +506,49 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
       cudaFreeAsync(hp, st);
     }
   }
+  cudaSetDevice(prev);
+  return err;
+}
+
+int nmfa_plan_run_sweeps(nmfa_plan_t* pl, uint64_t seed, int64_t r0, int32_t t_begin,
+                         int32_t t_end, int32_t energy_pass, int8_t* cfg, double* energy,
+                         void* stream) {
+  if (!pl) return arg_error("NULL plan");
+  const nmfa_problem* p = pl->p;
+  if (p->path != NMFA_PATH_DENSE) return arg_error("sweep ranges are a dense-path feature");
+  if (t_begin < 0 || t_end < t_begin || t_end > pl->t_f)
+    return arg_error("sweep range must satisfy 0 <= t_begin <= t_end <= t_f");
+  if (dense_is_sharded(p) && t_end - t_begin > 1)
+    return arg_error("a row-sharded problem runs one sweep per call (all-gather in between)");
+  if (energy_pass && !energy) return arg_error("energy pass needs an energy buffer");
+  if (energy_pass && !dense_energy_exact(p))
+    return arg_error("the tensor-core energy pass needs integer couplings with |J c| < 2^24");
+  if (energy_pass && t_end != pl->t_f)
+    return arg_error("the energy pass follows the last sweep (t_end == t_f)");
+  g_launches = 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  const int err = dense_run_sweeps(pl, seed + (uint64_t)r0, nullptr, nullptr, cfg, nullptr,
+                                   nullptr, energy, t_begin, t_end, energy_pass != 0,
+                                   (cudaStream_t)stream);
+  cudaSetDevice(prev);
+  return err;
+}
+
+int nmfa_plan_image_info(const nmfa_plan_t* pl, void** img0, void** img1, int64_t* slice_bytes,
+                         int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi) {
+  if (!pl || !img0 || !img1 || !slice_bytes || !n_slices || !slice_lo || !slice_hi)
+    return arg_error("NULL argument");
+  return dense_image_info(pl, img0, img1, slice_bytes, n_slices, slice_lo, slice_hi);
+}
+
+int nmfa_plan_read_config(const nmfa_plan_t* pl, int8_t* cfg, void* stream) {
+  if (!pl || !cfg) return arg_error("NULL argument");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->p->device);
+  const int err = dense_read_config(pl, cfg, (cudaStream_t)stream);
   cudaSetDevice(prev);
   return err;
 }
@@ -545,6 +647,9 @@ int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
 int nmfa_energy(const nmfa_problem_t* p, const int8_t* cfg, int64_t n_cfg, double* energy,
                 void* stream) {
   if (!p || !cfg || !energy) return arg_error("NULL argument");
+  if (p->device_generated)
+    return arg_error("a device-generated problem has no edge list; its energies come from "
+                     "the anneal's tensor-core energy pass");
   if (n_cfg < 1) return arg_error("need at least one configuration");
   cudaStream_t st = (cudaStream_t)stream;
   int prev = 0;

@@ -43,6 +43,13 @@ struct nmfa_problem {
   double j_scale = 1.0;    // J_dev = J / j_scale (power of two); inv_norm carries j_scale
   double max_row_abs = 0.0; // max_i sum_j |J_ij| (exactness bound of tensor-core energies)
   int32_t np = 0;          // n padded to a multiple of 16 (tensor-core paths)
+  // Row shard held on this device (dense path): spins [row_lo, row_hi) are the
+  // rows of J stored here and the spins this device updates; the B image has
+  // `brows` rows.  The whole problem is row_lo = 0, row_hi = n, brows = np.
+  int64_t row_lo = 0, row_hi = 0;
+  int32_t brows = 0;
+  bool device_generated = false;  // on-device SK couplings: no edge list / CSR
+  uint64_t sk_seed = 0;
 
   std::vector<double> h, norm_safe;  // host copies (float64)
 
@@ -109,6 +116,14 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         double* energy, bool* energy_done, cudaStream_t st);
 bool dense_energy_exact(const nmfa_problem* p);
+bool dense_is_sharded(const nmfa_problem* p);
+int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise, const float* s0,
+                     int8_t* cfg, float* s_out, float* s_hist, double* energy, int t_begin,
+                     int t_end, bool energy_pass, cudaStream_t st);
+int dense_image_info(const nmfa_plan* pl, void** img0, void** img1, int64_t* slice_bytes,
+                     int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi);
+int dense_read_config(const nmfa_plan* pl, int8_t* cfg, cudaStream_t st);
+int dense_problem_generate_sk(nmfa_problem* p, uint64_t seed);
 int dense_plan_alloc(nmfa_plan* pl);
 void dense_plan_free(nmfa_plan* pl);
 int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jdense_rowmajor);

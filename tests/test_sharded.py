@@ -1,0 +1,82 @@
+"""Row-sharded J (config 5) host logic on CPU: shard geometry, the Philox
+twin of the on-device SK generator (pinned to the published Random123
+known-answer vectors), and the in-place slice all-gather under gloo world 2."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import nmfa_oracle as O
+from paper_1806_08422_b200.sharded import exchange_slices, row_shard
+
+
+def test_row_shard_tiles_rows():
+    n, world = 65536, 8
+    spans = [row_shard(n, world, g) for g in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert all(lo % 128 == 0 for lo, _ in spans)
+    with pytest.raises(ValueError):
+        row_shard(1000, 2, 0)
+
+
+# Random123 philox4x32_10 known-answer vectors (kat_vectors: ctr, key -> out)
+PHILOX_KAT = [
+    ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", PHILOX_KAT)
+def test_philox_twin_known_answers(ctr, key, want):
+    got = O.philox4x32_10(*[np.array([c], np.uint32) for c in ctr], *key)
+    assert tuple(int(w[0]) for w in got) == want
+
+
+def test_sk_device_couplings_shape_and_balance():
+    J = O.sk_device_couplings(256, 5)
+    assert np.array_equal(J, J.T) and np.all(np.diag(J) == 0)
+    off = J[~np.eye(256, dtype=bool)]
+    assert set(np.unique(off)) == {-1.0, 1.0}
+    # fair coin: mean of 32,640 independent +-1 within 5 sigma
+    assert abs(off.mean()) < 5 / np.sqrt(off.size / 2)
+    assert not np.array_equal(J, O.sk_device_couplings(256, 6))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n_slices_per, sb, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = torch.full((world * n_slices_per * sb + 7,), 255, dtype=torch.uint8)
+        lo, hi = rank * n_slices_per, (rank + 1) * n_slices_per
+        mine = torch.arange(lo * sb, hi * sb, dtype=torch.int64) % 251
+        img[lo * sb: hi * sb] = mine.to(torch.uint8)
+        exchange_slices(img, lo, hi, sb)
+        out[rank] = img.numpy().copy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_slices_gathers_every_shard():
+    world, per, sb = 2, 3, 64
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), per, sb, out), nprocs=world, join=True)
+    want = (np.arange(world * per * sb) % 251).astype(np.uint8)
+    for g in range(world):
+        assert np.array_equal(out[g][: world * per * sb], want)
+        assert np.all(out[g][world * per * sb:] == 255)   # bytes past the slabs untouched
