@@ -419,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           }
           if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
         } else {
-          const bool extra = valid && (a.s_hist != nullptr || last);
+          const bool extra = valid && (a.s_hist != nullptr || (last && a.cfg != nullptr));
           auto do_chunk = [&](auto wtag, int c) {
             constexpr int W = decltype(wtag)::value;
             const int i0 = tl.n0 + c;
@@ -469,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
                 for (int cc = 0; cc < W; ++cc)
                   if (cc < nvalid) hrow[cc] = ms[cc];
               }
-              if (last) {
+              if (last && a.cfg) {
                 int8_t* crow = a.cfg + r * a.n + i0;
 #pragma unroll
                 for (int cc = 0; cc < W; ++cc)  // sign_round: s < 0 -> -1 else +1 (problem.py:181)
