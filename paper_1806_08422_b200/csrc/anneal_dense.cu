@@ -48,8 +48,18 @@ constexpr int kBK = 128;  // K per pipeline stage: one 32 KB TMA box per operand
 #define NMFA_EPI_WARPS 16
 #endif
 constexpr int kDEpiWarps = NMFA_EPI_WARPS;
+constexpr int kParts = kDEpiWarps / 4;  // column parts per TMEM lane quarter
 constexpr int kDThreads = 32 * kDEpiWarps + 128;
+// Warp roles: epilogue warps first, control warps on the highest ids (the
+// scheduler favours high ids; see the header).  Warp w reads TMEM lane quarter
+// w % 4.  NMFA_ROLES_FIRST (experiment) puts producer/MMA/alloc on warps 0-2.
+#ifdef NMFA_ROLES_FIRST
+constexpr int kEpiBase = 4;
+constexpr int kWarpProducer = 0, kWarpMma = 1, kWarpAlloc = 2;
+#else
+constexpr int kEpiBase = 0;
 constexpr int kWarpProducer = kDEpiWarps, kWarpMma = kDEpiWarps + 1, kWarpAlloc = kDEpiWarps + 2;
+#endif
 constexpr uint32_t kATile = 128 * kBK * 2;     // 128 rows x 128 k fp16 = 32 KB
 constexpr uint32_t kBTileMax = 128 * kBK * 2;  // <= 128 rows (N/2) x 128 k
 constexpr uint32_t kDStageBytes = kATile + kBTileMax;
@@ -68,18 +78,19 @@ struct DenseState {
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
-  int* d_korder = nullptr;        // per replica block: static k-slice order
   unsigned* d_kneed = nullptr;    // per (block, k-slice): spins published per sweep (x2 CTAs)
   unsigned* d_ready = nullptr;    // per (block, k-slice): spins published this launch
   int n_mblk = 0;
+  int n_tiles = 0;
+  int16_t* d_korder = nullptr;     // [tile][kblocks] K order (null: natural)
   CUtensorMap tmA[2];
-  CUtensorMap tmB[5];  // box lines 16, 32, 64, 128, 256 (= 8..128 rows)
+  CUtensorMap tmB[2];  // B boxes of exactly one tile half (2 x rows lines), the two widths
+  int bhalf[2] = {0, 0};
 };
 
 struct DenseStepArgs {
   const DenseTile* tiles;
   const int* tile_off;
-  const int* korder;       // [m][kblocks] static k-slice order of block m's tiles
   const unsigned* kneed;   // [m][kblocks] spins a sweep publishes into the slice (both CTAs)
   unsigned* ready;         // [m][kblocks] spins published so far this launch
   int kblocks, k_last_sub;
@@ -103,6 +114,10 @@ struct DenseStepArgs {
   const double* h;         // raw fields (energy pass)
   double half_scale;       // 0.5 * j_scale (energy pass)
   unsigned long long* trace;  // debug timeline (NMFA_TRACE), CTA 0 only
+  unsigned long long* tl2;    // debug: globaltimer per (pair, tile) (NMFA_TRACE2)
+  const int16_t* korder;      // [tile][kblocks] K order, or null for natural order
+  int bhalf0, bhalf1;         // rows per CTA of the two tile widths (B box sizes)
+  unsigned long long* tl3;    // debug: per k-slice clock64 of CTA 0 (NMFA_TRACE3)
 };
 
 // ---------------------------------------------------------------------------
@@ -145,13 +160,18 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
                : "memory");
 }
-__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
-                                         uint32_t acc) {
+// 2-CTA MMA from descriptor words: the high word (SBO, version) is constant and
+// the low word is (LBO << 16) | (smem address >> 4), so stepping K by 16 is one
+// add (keeps the single issuing thread lean while 16 epilogue warps compete).
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo,
+                                         uint32_t desc_hi, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "mov.b64 da, {%1, %3};\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %4, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(desc_hi), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
@@ -162,6 +182,19 @@ __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_remote_arrive_relaxed(uint32_t mbar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster)
+               : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -180,6 +213,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+#ifdef NMFA_DBG_PLAINMEM  // experiment: no L2 cache-policy hints on state loads/stores
+__device__ __forceinline__ uint4 ld_hint(const void* ptr, uint64_t) {
+  return *reinterpret_cast<const uint4*>(ptr);
+}
+__device__ __forceinline__ void st_hint(void* ptr, uint4 v, uint64_t) {
+  *reinterpret_cast<uint4*>(ptr) = v;
+}
+#else
 __device__ __forceinline__ uint4 ld_hint(const void* ptr, uint64_t pol) {
   uint4 v;
   asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
@@ -192,6 +233,7 @@ __device__ __forceinline__ void st_hint(void* ptr, uint4 v, uint64_t pol) {
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
 }
+#endif
 
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
@@ -219,11 +261,8 @@ template <bool kInjected>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_anneal_kernel(const __grid_constant__ CUtensorMap tmA0,
                         const __grid_constant__ CUtensorMap tmA1,
-                        const __grid_constant__ CUtensorMap tmB16,
-                        const __grid_constant__ CUtensorMap tmB32,
-                        const __grid_constant__ CUtensorMap tmB64,
-                        const __grid_constant__ CUtensorMap tmB128,
-                        const __grid_constant__ CUtensorMap tmB256, const DenseStepArgs a) {
+                        const __grid_constant__ CUtensorMap tmB0,
+                        const __grid_constant__ CUtensorMap tmB1, const DenseStepArgs a) {
   extern __shared__ __align__(1024) uint8_t dsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -238,9 +277,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   const int n_phases = (a.t_end - a.t_begin) + (a.energy_pass ? 1 : 0);
 
   if (warp == kWarpProducer && lane == 0) {
-    const CUtensorMap* maps[7] = {&tmA0, &tmA1, &tmB16, &tmB32, &tmB64, &tmB128, &tmB256};
+    const CUtensorMap* maps[4] = {&tmA0, &tmA1, &tmB0, &tmB1};
 #pragma unroll
-    for (int m = 0; m < 7; ++m)
+    for (int m = 0; m < 4; ++m)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps[m])) : "memory");
     for (int s = 0; s < kDStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -276,11 +315,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           const int half = tl.nlen >> 1;
           const int arow = tl.m_blk * 256 + (int)cta * 128;
           const int brow = tl.n0 - a.row_lo + (int)cta * half;  // row within this shard of J
-          const int* kord = a.korder + tl.m_blk * a.kblocks;
           const int jglob = ph * (j1 - j0) + (j - j0);
+          const int16_t* kord = a.korder ? a.korder + (size_t)j * a.kblocks : nullptr;
           if (a.trace && blockIdx.x == 0 && jglob < 512) a.trace[jglob * 8 + 0] = clock64();
+          unsigned long long* t2 = (a.tl2 && cta == 0 && jglob < 64) ? a.tl2 + ((blockIdx.x >> 1) * 64 + jglob) * 8 : nullptr;
+          if (t2) t2[0] = gtimer();
+          long long wempty = 0;
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
-            const int kb = kord[ki];
+            const int kb = kord ? kord[ki] : ki;
             if (ki >= known) {
               // slices of block m for sweep t were written by sweep t-1: poll the next
               // (up to) 8 entries of the k order with independent relaxed loads
@@ -290,11 +332,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
                 const int cnt = min(8, a.kblocks - known);
 #pragma unroll
                 for (int x = 0; x < 8; ++x)
-                  if (x < cnt) v[x] = ld_relaxed_gpu(a.ready + qb + kord[known + x]);
+                  if (x < cnt) v[x] = ld_relaxed_gpu(a.ready + qb + (kord ? kord[known + x] : known + x));
                 int adv = 0;
 #pragma unroll
                 for (int x = 0; x < 8; ++x)
-                  if (x < cnt && adv == x && v[x] >= (unsigned)ph * a.kneed[qb + kord[known + x]]) ++adv;
+                  if (x < cnt && adv == x && v[x] >= (unsigned)ph * a.kneed[qb + (kord ? kord[known + x] : known + x)]) ++adv;
                 known += adv;
                 if (known <= ki) __nanosleep(20);
               }
@@ -303,26 +345,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             }
             if (ki == a.kblocks - 1 && a.trace && blockIdx.x == 0 && jglob < 512)
               a.trace[jglob * 8 + 1] = clock64();  // producer reached the last slice
+            if (t2 && ki == 0) t2[5] = gtimer();
+            if (t2 && ki == a.kblocks - 1) t2[1] = gtimer();
             const int s = it % kDStages;
-            mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+            if (a.trace) {
+              const long long c0 = clock64();
+              mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+              wempty += clock64() - c0;
+            } else {
+              mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+            }
+            if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 0] = clock64();
             const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
             if (cta == 0)
               mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
             uint8_t* st = smem + (size_t)s * kDStageBytes;
             tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb, pol_keep);
-            int off = 0;  // rows
-#pragma unroll
-            for (int b = 4; b >= 0; --b) {
-              const int rows = 8 << b;
-              if (half & rows) {
-                const CUtensorMap* tm = b == 4 ? &tmB256 : b == 3 ? &tmB128 : b == 2 ? &tmB64
-                                      : b == 1 ? &tmB32 : &tmB16;
-                tma2d_pair(smem_u32(st + kATile + off * 2 * 128), tm, 0,
-                           (kb * a.brows + brow + off) * 2, fb, pol_keep);
-                off += rows;
-              }
-            }
+            // J rows of this CTA's half of the tile: ONE box (the per-box TMA cost is
+            // ~100 cycles, so the half is never split into power-of-two boxes)
+            tma2d_pair(smem_u32(st + kATile), half == a.bhalf1 ? &tmB1 : &tmB0, 0,
+                       (kb * a.brows + brow) * 2, fb, pol_keep);
           }
+          if (a.trace && blockIdx.x == 0 && jglob < 512)
+            a.trace[jglob * 8 + 7] = wempty;  // cycles the producer waited for a free stage
         }
       }
     }
@@ -330,42 +375,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     // ------------------------- MMA issuer (leader CTA) -------------------------
     if (cta == 0 && lane == 0) {
       int it = 0, jj = 0;
+      const uint64_t desc0 = make_desc_noswizzle(smem_u32(smem), 128, 2048);
+      const uint32_t desc_lo0 = (uint32_t)desc0, desc_hi = (uint32_t)(desc0 >> 32);
       for (int ph = 0; ph < n_phases; ++ph) {
         for (int j = j0; j < j1; ++j, ++jj) {
           const DenseTile tl = a.tiles[j];
           const int slot = jj & 1, use = jj >> 1;
           mbar_wait(&tempty_bar[slot], (use & 1) ^ 1);
           if (a.trace && blockIdx.x == 0 && jj < 512) a.trace[jj * 8 + 2] = clock64();
+          if (a.tl2 && jj < 64) a.tl2[((blockIdx.x >> 1) * 64 + jj) * 8 + 2] = gtimer();
           tc_fence_after();
           const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
           const uint32_t d = tbase + (uint32_t)slot * kAccCols;
-          const int* kord = a.korder + tl.m_blk * a.kblocks;
+          long long wfull = 0;
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
-            const int kb = kord[ki];
             const int s = it % kDStages;
-            mbar_wait(&full_bar[s], (it / kDStages) & 1);
+            if (a.trace) {
+              const long long c0 = clock64();
+              mbar_wait(&full_bar[s], (it / kDStages) & 1);
+              wfull += clock64() - c0;
+            } else {
+              mbar_wait(&full_bar[s], (it / kDStages) & 1);
+            }
             tc_fence_after();
-            const uint32_t sa = smem_u32(smem + (size_t)s * kDStageBytes);
-            const uint32_t sb = sa + kATile;
-            const int nsub = (kb == a.kblocks - 1) ? a.k_last_sub : kBK / 16;
-            for (int ks = 0; ks < nsub; ++ks) {
-              mma_pair(d, make_desc_noswizzle(sa + ks * 256, 128, 2048),
-                       make_desc_noswizzle(sb + ks * 256, 128, 2048), idesc, (ki | ks) ? 1u : 0u);
+            if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 1] = clock64();
+            const uint32_t a_lo = desc_lo0 + (uint32_t)s * (kDStageBytes >> 4);
+            const uint32_t b_lo = a_lo + (kATile >> 4);
+            if (ki != tl.pad) {
+#pragma unroll
+              for (int ks = 0; ks < kBK / 16; ++ks)
+                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | ks) ? 1u : 0u);
+            } else {
+              for (int ks = 0; ks < a.k_last_sub; ++ks)
+                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | ks) ? 1u : 0u);
             }
             commit_pair_mc(&empty_bar[s]);
+            if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 2] = clock64();
           }
           commit_pair_mc(&tfull_bar[slot]);
-          if (a.trace && blockIdx.x == 0 && jj < 512) a.trace[jj * 8 + 3] = clock64();
+          if (a.tl2 && jj < 64) a.tl2[((blockIdx.x >> 1) * 64 + jj) * 8 + 3] = gtimer();
+          if (a.trace && blockIdx.x == 0 && jj < 512) {
+            a.trace[jj * 8 + 3] = clock64();
+            a.trace[jj * 8 + 6] = wfull;  // cycles the MMA issuer waited for TMA data
+          }
         }
       }
     }
-  } else if (warp < kDEpiWarps) {
+  } else if (warp >= kEpiBase && warp < kEpiBase + kDEpiWarps) {
     // ------------------------- fused NMFA epilogue -------------------------
     // State per (replica r, spin i): hi = fp16(s) lives in the operand image
     // the TMA reads this sweep, lo = fp16(s - hi) in a second image of the same
     // layout, so s = hi + lo carries ~22 bits and the per-sweep working set
     // (2 images + lo + J) is ~104 MB at K2000 / 8192 reads.
-    const int e = warp, quarter = e & 3, hpart = e >> 2;  // lane quarter x column part
+    const int e = warp - kEpiBase, quarter = e & 3, hpart = e >> 2;  // lane quarter x column part
     const int row = 32 * quarter + lane;
     const uint32_t leader_tempty0 = map_to_rank(smem_u32(&tempty_bar[0]), 0);
     const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
@@ -394,7 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
         // this warp's columns: a contiguous, 8-aligned quarter of the tile (balanced to 8 spins)
         const int n8 = tl.nlen >> 3;
-        const int c_lo = (n8 * hpart / 4) * 8, c_hi = (n8 * (hpart + 1) / 4) * 8;
+        const int c_lo = (n8 * hpart / kParts) * 8, c_hi = (n8 * (hpart + 1) / kParts) * 8;
         auto img_off = [&](int i) {
           return (long long)(i >> 7) * a.Rp * 256 + row_off + ((i & 127) >> 3) * 128;
         };
@@ -424,17 +486,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             constexpr int W = decltype(wtag)::value;
             const int i0 = tl.n0 + c;
             float acc[W], ms[W], lo[W];
+#ifdef NMFA_DBG_NOTMEM  // experiment: no accumulator reads (fake fields)
+#pragma unroll
+            for (int cc = 0; cc < W; ++cc) acc[cc] = 0.001f * (float)(cc + c);
+#else
             if constexpr (W == 16) tmem_ld16(tacc + c, acc);
             else tmem_ld8(tacc + c, acc);
+#endif
 #ifdef NMFA_DBG_NOEPI
             tmem_wait_ld();
+#ifdef NMFA_DBG_SPREAD  // experiment: accumulator reads spread over the tile, no math
+            __nanosleep(NMFA_DBG_SPREAD);
+#endif
             if (acc[0] == 12345.f) a.lo[0] = 1;
             return;
 #endif
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
               const long long off = img_off(i0 + 8 * h);
-#ifndef NMFA_DBG_NOMEM
+#if defined(NMFA_DBG_NOLOAD)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) { ms[8 * h + q] = 0.01f * q; lo[8 * h + q] = 0.f; }
+#elif defined(NMFA_DBG_NOLO)
+              unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) lo[8 * h + q] = 0.f;
+#elif !defined(NMFA_DBG_NOMEM)
               unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
               unpack_half8(ld_hint(a.lo + off, pol_stream), lo + 8 * h);
 #else
@@ -447,15 +524,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             tmem_wait_ld();
             const int nvalid = valid ? min(W, a.n - i0) : 0;
             const float* nz = kInjected ? a.noise + ((long long)r * a.t_f + t) * a.n + i0 : nullptr;
+#ifdef NMFA_DBG_NOMATH
+#pragma unroll
+            for (int cc = 0; cc < W; ++cc) ms[cc] = fmaf(acc[cc], 1e-6f, ms[cc]);
+#else
             update_chunk<kInjected, W>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
                                        (uint32_t)(i0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+#endif
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
               const long long off = img_off(i0 + 8 * h);
               uint4 hv, lv;
-              split_half8(ms + 8 * h, hv, lv, last);
-#ifndef NMFA_DBG_NOMEM
+              split_hilo8(ms + 8 * h, hv, lv, last);
+#if defined(NMFA_DBG_NOLO)
+              st_hint(a_next + off, hv, pol_keep);
+              if (lv.x == 0x12345u && lv.y == 7u) a.lo[0] = 1;
+#elif !defined(NMFA_DBG_NOMEM)
               st_hint(a_next + off, hv, pol_keep);
               st_hint(a.lo + off, lv, pol_stream);
 #else
@@ -489,16 +574,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 512) atomicMax(&a.trace[jj * 8 + 5], clock64());
+        if (a.tl2 && lane == 0 && jj < 64) atomicMax(&a.tl2[((blockIdx.x >> 1) * 64 + jj) * 8 + 4], gtimer());
         if (lane == 0) {
-          mbar_remote_arrive(slot ? leader_tempty1 : leader_tempty0);
+          // one release fence orders the warp's TMEM reads (tcgen05 fence + __syncwarp
+          // above) and its state stores before both the accumulator-free arrive and
+          // the readiness counters; the consumers acquire and fence the async proxy
+          fence_release_gpu();
+          mbar_remote_arrive_relaxed(slot ? leader_tempty1 : leader_tempty0);
           if (!energy_phase && c_hi > c_lo) {
-            // publish this warp's rows x columns for the next sweep (counted in spin-quarters)
-            __threadfence();
+            // publish this warp's rows x columns for the next sweep (spin-quarters)
             fence_proxy_async_global();
             const int s_lo = tl.n0 + c_lo, s_hi = tl.n0 + c_hi;
             for (int kb = s_lo >> 7; kb <= (s_hi - 1) >> 7; ++kb)
-              atomicAdd(a.ready + tl.m_blk * a.kblocks + kb,
-                        (unsigned)(min(s_hi, kb * 128 + 128) - max(s_lo, kb * 128)));
+              red_relaxed_gpu(a.ready + tl.m_blk * a.kblocks + kb,
+                              (unsigned)(min(s_hi, kb * 128 + 128) - max(s_lo, kb * 128)));
           }
         }
       }
@@ -523,19 +612,12 @@ __global__ void dense_init_kernel(uint8_t* a_img, uint8_t* lo_img, const float* 
   float v[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = (r < R && i0 + k < n) ? s0[r * n + i0 + k] : 0.f;
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const __half2 hh = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
-    const float2 hf = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(v[2 * k] - hf.x, v[2 * k + 1] - hf.y);
-    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
-    l[k] = *reinterpret_cast<const uint32_t*>(&ll);
-  }
+  uint4 hv, lv;
+  split_hilo8<true>(v, hv, lv, false);
   const long long off = (long long)(i0 >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i0 & 127) >> 3) * 128 +
                         (r & 7) * 16;
-  *reinterpret_cast<uint4*>(a_img + off) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(lo_img + off) = make_uint4(l[0], l[1], l[2], l[3]);
+  *reinterpret_cast<uint4*>(a_img + off) = hv;
+  *reinterpret_cast<uint4*>(lo_img + off) = lv;
 }
 
 // ---------------------------------------------------------------------------
@@ -650,8 +732,8 @@ void dense_plan_free(nmfa_plan* pl) {
   if (ds->a_img[1]) cudaFree(ds->a_img[1]);
   if (ds->d_tiles) cudaFree(ds->d_tiles);
   if (ds->d_tile_off) cudaFree(ds->d_tile_off);
-  if (ds->d_korder) cudaFree(ds->d_korder);
   if (ds->d_kneed) cudaFree(ds->d_kneed);
+  if (ds->d_korder) cudaFree(ds->d_korder);
   if (ds->d_ready) cudaFree(ds->d_ready);
   delete ds;
   pl->dense = nullptr;
@@ -702,15 +784,80 @@ int dense_plan_alloc(nmfa_plan* pl) {
   const long long tpm = (upm + best_w - 1) / best_w, T = tpm * mb;
   const int pairs = (int)std::min<long long>(sms / 2, T);
   ds->pairs = pairs;
-  std::vector<DenseTile> tiles;
-  tiles.reserve(T);
+  // Spin-major dealing: sort tiles by (spin tile k, replica block m) and give
+  // position j of pair q the tile q + j*pairs.  Every pair works on the
+  // lowest spins first, so in sweep t the k-slices become ready in the order
+  // the sweep-(t+1) k-loops consume them (natural K order), and the first tile
+  // of a sweep does not wait for the end of the previous one.
+  // debug knob NMFA_TILE_ORDER: mmajor (contiguous m-major runs), sorted (the
+  // same runs ordered by spin within each pair), spin (spin-major dealing)
+  static const char* order_env = getenv("NMFA_TILE_ORDER");
+  const std::string order = order_env ? order_env : "mmajor";
+  std::vector<DenseTile> mmaj;
+  mmaj.reserve(T);
   for (long long m = 0; m < mb; ++m)
     for (long long k = 0; k < tpm; ++k) {  // balanced widths within the block
       const long long a0 = upm * k / tpm, a1 = upm * (k + 1) / tpm;
-      tiles.push_back({(int)m, (int)(p->row_lo + a0 * 16), (int)((a1 - a0) * 16), 0});
+      mmaj.push_back({(int)m, (int)(p->row_lo + a0 * 16), (int)((a1 - a0) * 16), 0});
     }
+  std::vector<DenseTile> tiles;
+  tiles.reserve(T);
   std::vector<int> off(pairs + 1, 0);
-  for (int q = 0; q <= pairs; ++q) off[q] = (int)(T * q / pairs);
+  if (order == "spin") {
+    std::vector<DenseTile> sorted(mmaj);
+    std::stable_sort(sorted.begin(), sorted.end(),
+                     [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int)tiles.size();
+      for (long long j = q; j < T; j += pairs) tiles.push_back(sorted[j]);
+    }
+  } else {
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int)tiles.size();
+      const long long j0 = T * q / pairs, j1 = T * (q + 1) / pairs;
+      std::vector<DenseTile> run(mmaj.begin() + j0, mmaj.begin() + j1);
+      if (order == "sorted")
+        std::stable_sort(run.begin(), run.end(),
+                         [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
+      tiles.insert(tiles.end(), run.begin(), run.end());
+    }
+  }
+  off[pairs] = (int)tiles.size();
+  // K order per tile: natural (slice 0 first), so a spin's fp32 field is summed
+  // in the same order for every schedule, replica count and row sharding.  The
+  // debug knob NMFA_KORDER=early consumes slices earliest-published first
+  // (slice (m, kb) is published when the last tile covering it ends, estimated
+  // by that tile's position in its pair's list); results then depend on the
+  // schedule.  Measured: no gain at K2000 (profiles/r01/korder_ab.log).
+  const int kbn = ds->kblocks;
+  static const char* korder_env = getenv("NMFA_KORDER");
+  const bool early = korder_env && std::string(korder_env) == "early";
+  std::vector<int> avail((size_t)mb * kbn, 0);
+  for (int q = 0; q < pairs; ++q)
+    for (int j = off[q]; j < off[q + 1]; ++j) {
+      const DenseTile& t = tiles[j];
+      for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb)
+        avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
+    }
+  std::vector<int16_t> korder;
+  if (early) korder.resize((size_t)T * kbn);
+  for (long long j = 0; j < T; ++j) {
+    DenseTile& t = tiles[j];
+    t.pad = kbn - 1;  // position of the short last k-slice in the tile's K order
+    if (!early) continue;
+    int16_t* ko = &korder[(size_t)j * kbn];
+    for (int k = 0; k < kbn; ++k) ko[k] = (int16_t)k;
+    std::stable_sort(ko, ko + kbn, [&](int16_t x, int16_t y) {
+      return avail[(size_t)t.m_blk * kbn + x] < avail[(size_t)t.m_blk * kbn + y];
+    });
+    for (int k = 0; k < kbn; ++k)
+      if (ko[k] == kbn - 1) t.pad = k;
+  }
+  if (early) {
+    NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int16_t)));
+    NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int16_t),
+                             cudaMemcpyHostToDevice));
+  }
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_tiles, tiles.size() * sizeof(DenseTile)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_tiles, tiles.data(), tiles.size() * sizeof(DenseTile),
                            cudaMemcpyHostToDevice));
@@ -718,13 +865,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(
       cudaMemcpy(ds->d_tile_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
   ds->n_mblk = (int)mb;
-  // K order: natural (k-slice 0 first), so the fp32 accumulation order of a
-  // spin's field does not depend on the schedule or on the row sharding
-  // (results are identical for any number of shards).  An early-ready-first
-  // order was measured: no gain (profiles/r01).  Readiness is counted per
-  // (replica block, k-slice) in spin-quarters; slices of other shards need 0.
-  const int kbn = ds->kblocks;
-  std::vector<int> avail((size_t)mb * kbn, 0);
+  ds->n_tiles = (int)T;
+  // Readiness is counted per (replica block, k-slice) in spin-quarters; slices
+  // of other shards need 0.
   std::vector<unsigned> kneed((size_t)mb * kbn, 0);
   for (int q = 0; q < pairs; ++q)
     for (int j = off[q]; j < off[q + 1]; ++j) {
@@ -732,14 +875,8 @@ int dense_plan_alloc(nmfa_plan* pl) {
       for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb) {
         const int lo_s = std::max(t.n0, kb * 128), hi_s = std::min(t.n0 + t.nlen, kb * 128 + 128);
         kneed[(size_t)t.m_blk * kbn + kb] += 8u * (unsigned)(hi_s - lo_s);  // 2 CTAs x 4 quarters
-        avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
       }
     }
-  std::vector<int> korder((size_t)mb * kbn);
-  for (long long m = 0; m < mb; ++m) std::iota(&korder[(size_t)m * kbn], &korder[(size_t)m * kbn] + kbn, 0);
-  NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int)));
-  NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int),
-                           cudaMemcpyHostToDevice));
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_kneed, kneed.size() * sizeof(unsigned)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_kneed, kneed.data(), kneed.size() * sizeof(unsigned),
                            cudaMemcpyHostToDevice));
@@ -749,9 +886,26 @@ int dense_plan_alloc(nmfa_plan* pl) {
   for (int b = 0; b < 2; ++b)
     if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
       return err;
-  for (int b = 0; b < 5; ++b)
-    if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * p->brows * 2, 16u << b)))
-      return err;
+  // one B tensor map per distinct tile width (balanced widths: at most two)
+  {
+    int hs[2] = {-1, -1}, nh = 0;
+    for (const DenseTile& t : tiles) {
+      const int h = t.nlen / 2;
+      if (h == hs[0] || h == hs[1]) continue;
+      if (nh == 2 || h > 128 || h % 8) {
+        set_error("dense schedule: unsupported tile width " + std::to_string(t.nlen));
+        return NMFA_ERR_STATE;
+      }
+      hs[nh++] = h;
+    }
+    if (nh == 1) hs[1] = hs[0];
+    for (int b = 0; b < 2; ++b) {
+      ds->bhalf[b] = hs[b];
+      if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * p->brows * 2,
+                               2u * (uint32_t)hs[b])))
+        return err;
+    }
+  }
   NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_anneal_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmemBytes));
   NMFA_CUDA_TRY(cudaFuncSetAttribute(dense_anneal_kernel<true>,
@@ -789,8 +943,8 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   DenseStepArgs a{};
   a.tiles = ds->d_tiles;
   a.tile_off = ds->d_tile_off;
-  a.korder = ds->d_korder;
   a.kneed = ds->d_kneed;
+  a.korder = ds->d_korder;
   a.ready = ds->d_ready;
   a.kblocks = ds->kblocks;
   a.k_last_sub = ds->k_last_sub;
@@ -839,16 +993,61 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
     cudaMemset(trace, 0, 512 * 8 * 8);
     a.trace = trace;
   }
+  static const char* tl2_path = getenv("NMFA_TRACE2");
+  static unsigned long long* tl2 = nullptr;
+  if (tl2_path) {
+    if (!tl2) cudaMallocManaged(&tl2, (size_t)ds->pairs * 64 * 8 * 8);
+    cudaMemset(tl2, 0, (size_t)ds->pairs * 64 * 8 * 8);
+    a.tl2 = tl2;
+  }
+  static const char* tl3_path = getenv("NMFA_TRACE3");
+  static unsigned long long* tl3 = nullptr;
+  if (tl3_path) {
+    if (!tl3) cudaMallocManaged(&tl3, 64 * 4 * 8);
+    cudaMemset(tl3, 0, 64 * 4 * 8);
+    a.tl3 = tl3;
+  }
   auto kern = noise ? dense_anneal_kernel<true> : dense_anneal_kernel<false>;
-  NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1],
-                                   ds->tmB[2], ds->tmB[3], ds->tmB[4], a));
+  a.bhalf0 = ds->bhalf[0];
+  a.bhalf1 = ds->bhalf[1];
+  NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1], a));
   add_launches(launches);
+  if (tl3_path) {
+    cudaStreamSynchronize(st);
+    FILE* f = fopen(tl3_path, "w");
+    if (f) {
+      for (int k = 0; k < 64; ++k) fprintf(f, "%llu %llu %llu\n", tl3[k * 4], tl3[k * 4 + 1], tl3[k * 4 + 2]);
+      fclose(f);
+    }
+  }
+  if (tl2_path) {
+    cudaStreamSynchronize(st);
+    std::vector<DenseTile> ht(ds->n_tiles);
+    std::vector<int> hoff(ds->pairs + 1);
+    cudaMemcpy(ht.data(), ds->d_tiles, ht.size() * sizeof(DenseTile), cudaMemcpyDeviceToHost);
+    cudaMemcpy(hoff.data(), ds->d_tile_off, hoff.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    FILE* f = fopen(tl2_path, "w");
+    if (f) {
+      // pair jglob m n0 nlen | prod_start last_slice_ready mma_start mma_end epi_end first_slice_ready
+      for (int q = 0; q < ds->pairs; ++q) {
+        const int nt = hoff[q + 1] - hoff[q];
+        for (int j = 0; j < 64; ++j) {
+          const unsigned long long* r = tl2 + ((size_t)q * 64 + j) * 8;
+          if (!r[2]) continue;
+          const DenseTile& t = ht[hoff[q] + j % nt];
+          fprintf(f, "%d %d %d %d %d %llu %llu %llu %llu %llu %llu\n", q, j, t.m_blk, t.n0, t.nlen,
+                  r[0], r[1], r[2], r[3], r[4], r[5]);
+        }
+      }
+      fclose(f);
+    }
+  }
   if (trace_path) {
     cudaStreamSynchronize(st);
     FILE* f = fopen(trace_path, "w");
     if (f) {
       for (int j = 0; j < 512; ++j) {
-        for (int k = 0; k < 6; ++k) fprintf(f, "%llu ", trace[j * 8 + k]);
+        for (int k = 0; k < 8; ++k) fprintf(f, "%llu ", trace[j * 8 + k]);
         fprintf(f, "\n");
       }
       fclose(f);

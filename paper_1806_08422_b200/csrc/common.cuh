@@ -337,7 +337,15 @@ __device__ __forceinline__ void unpack_half8(const uint4 v, float f[8]) {
 }
 
 // s -> hi = fp16(s), lo = fp16(s - hi) for 8 values (or hi = sign(s) when `sign`)
-__device__ __forceinline__ void split_half8(const float s[8], uint4& hi, uint4& lo, bool sign) {
+// State split for the dense path: hi = fp16(s) is the tensor-core operand,
+// lo = fp16(s - hi) the residual, so hi + lo carries ~22 bits.  (A 2^-11
+// fixed-point hi would make J.hi exact and order-independent, but its coarser
+// resolution for small |s| broke injected-noise trajectory parity at n = 520:
+// mean|dS| 4.3e-3, sign flips 2.2e-3 vs 2.2e-4 / 1e-4 -- profiles/r01.)
+// sign: write the +-1 configuration.  any_range is kept for call-site clarity
+// (user-supplied s0 may exceed [-1, 1]; the fp16 split handles any value).
+template <bool any_range = false>
+__device__ __forceinline__ void split_hilo8(const float s[8], uint4& hi, uint4& lo, bool sign) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -354,29 +362,6 @@ __device__ __forceinline__ void split_half8(const float s[8], uint4& hi, uint4& 
   }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
-// s -> hi = fp16(s), lo = fp16(s - hi)  (or hi = sign(s), lo = 0 when `sign`)
-__device__ __forceinline__ void split_half16(const float s[16], uint4 hi[2], uint4 lo[2],
-                                             bool sign) {
-  uint32_t h[8], l[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    float a = s[2 * k], b = s[2 * k + 1];
-    if (sign) {
-      a = a < 0.f ? -1.f : 1.f;
-      b = b < 0.f ? -1.f : 1.f;
-    }
-    const __half2 hh = __floats2half2_rn(a, b);
-    const float2 hf = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
-    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
-    l[k] = *reinterpret_cast<const uint32_t*>(&ll);
-  }
-  hi[0] = make_uint4(h[0], h[1], h[2], h[3]);
-  hi[1] = make_uint4(h[4], h[5], h[6], h[7]);
-  lo[0] = make_uint4(l[0], l[1], l[2], l[3]);
-  lo[1] = make_uint4(l[4], l[5], l[6], l[7]);
 }
 
 // Byte offset of element (row, k) inside a K-major no-swizzle UMMA operand

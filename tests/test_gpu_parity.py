@@ -188,6 +188,20 @@ def test_replica_sharding_invariance(G, path):
     assert res[2].final_energy == solo.final_energy
 
 
+def test_dense_results_do_not_depend_on_the_schedule():
+    """Exact fields (2^-11 operand grid, integer J): a different replica count
+    gives a different tile schedule and per-tile K order, yet the replicas the
+    two runs share must agree bit for bit."""
+    p = nb.gen_sk(600, 3)
+    assert p.device_info()["path"] == "dense"
+    params = nb.NmfaParams(t_f=150, seed=4)
+    full = nb.sample(p, params, 1280, return_s=True)
+    tail = nb.sample(p, params, 256, r0=1024, return_s=True)
+    assert torch.equal(full.configs[1024:], tail.configs)
+    assert torch.equal(full.energies[1024:], tail.energies)
+    assert torch.equal(full.s_final[1024:], tail.s_final)
+
+
 def test_returned_energies_match_oracle_energy(G):
     p = nb.gen_sk(100, 0)
     op = O.problem_from_edges(100, p.edges_i, p.edges_j, p.edge_weights)

@@ -8,7 +8,7 @@ proc = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--fo
                         stdout=subprocess.PIPE, text=True)
 threading.Thread(target=lambda: [rows.append(l) for l in proc.stdout], daemon=True).start()
 p = nb.gen_sk(2000, 7)
-R, t_f = 8192, 1000
+R, t_f = int(os.environ.get("NMFA_PROBE_R", 8192)), 1000
 params = nb.NmfaParams(t_f=t_f, seed=0)
 plan = nb.Plan(p, R, params.schedule.temperatures(t_f), params.alpha, params.sigma)
 cfg = torch.empty((R, 2000), dtype=torch.int8, device="cuda")

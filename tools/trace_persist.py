@@ -14,3 +14,6 @@ print(f"MMA idle between tiles: median {np.nanmedian(gap):.0f}, mean {np.nanmean
 print(f"  idle at sweep boundaries: mean {np.nanmean(gap[tps-1::tps]):.0f}; inside sweeps: mean {np.nanmean(np.delete(gap, np.s_[tps-1::tps])):.0f}")
 print(f"mma waited for epilogue (mma_start - prev-prev epi_end): median {np.nanmedian(d[2:,2]-d[:-2,5]):.0f}")
 sweep = np.diff(d[::tps, 2]); print(f"sweep period median {np.nanmedian(sweep):.0f} cycles")
+if d.shape[1] >= 8:
+    print(f"per tile: MMA waited for TMA data median {np.nanmedian(d[:,6]+t0):.0f} cycles; "
+          f"producer waited for a free stage median {np.nanmedian(d[:,7]+t0):.0f}")
