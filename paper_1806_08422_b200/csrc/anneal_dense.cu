@@ -781,6 +781,8 @@ int dense_plan_alloc(nmfa_plan* pl) {
       best_w = w;
     }
   }
+  static const char* w_env = getenv("NMFA_TILE_W");  // experiment: force the tile width
+  if (w_env && atoi(w_env) >= 1 && atoi(w_env) <= 16) best_w = atoi(w_env);
   const long long tpm = (upm + best_w - 1) / best_w, T = tpm * mb;
   const int pairs = (int)std::min<long long>(sms / 2, T);
   ds->pairs = pairs;

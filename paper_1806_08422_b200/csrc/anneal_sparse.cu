@@ -62,9 +62,8 @@ __global__ void __launch_bounds__(256) sparse_step_kernel(const SparseStepArgs a
     }
   } else {
     const unsigned long long key = a.key_base + (unsigned long long)r;
-    normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t, z);
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq) z[qq] *= a.sigma;
+    normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
+            bm_scale(a.sigma), z);
   }
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) {

@@ -91,11 +91,13 @@ __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32
   const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
-    const uint64_t p0 = (uint64_t)M0 * c0;  // IMAD.WIDE.U32
-    const uint64_t p1 = (uint64_t)M1 * c2;
-    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ (K.k0 + (uint32_t)i * 0x9E3779B9u);
-    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ (K.k1 + (uint32_t)i * 0xBB67AE85u);
-    c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
+    // 32-bit hi/lo products (no 64-bit register pairs: under the epilogue's
+    // register cap the paired IMAD.WIDE form costs an extra copy per product)
+    const uint32_t h0 = __umulhi(M0, c0), l0 = M0 * c0;
+    const uint32_t h1 = __umulhi(M1, c2), l1 = M1 * c2;
+    const uint32_t n0 = h1 ^ c1 ^ (K.k0 + (uint32_t)i * 0x9E3779B9u);
+    const uint32_t n2 = h0 ^ c3 ^ (K.k1 + (uint32_t)i * 0xBB67AE85u);
+    c0 = n0; c1 = l1; c2 = n2; c3 = l0;
   }
   return {c0, c1, c2, c3};
 }
@@ -105,24 +107,27 @@ constexpr uint32_t kNoiseTag = 0x4E4D4641u;
 // Box-Muller on ONE 32-bit word: the top 20 bits give u1 = (k + 1/2) 2^-20 in
 // (0, 1) (never 0 or 1, tail bound |z| <= 5.40), the low 12 bits the angle
 // u2 = k 2^-12 (equispaced angles: E[cos^2] = 1/2, E[cos^4] = 3/8 exactly).
-__device__ __forceinline__ void box_muller(uint32_t w, float& z0, float& z1) {
+// sigma is folded into the radius: r = sqrt(lgs * lg2(u1)) with
+// lgs = -2 ln 2 sigma^2 = sigma * sqrt(-2 ln u1); sigma = 0 gives z = +-0.
+__device__ __forceinline__ void box_muller(uint32_t w, float lgs, float& z0, float& z1) {
   const float u1 = fmaf((float)(w >> 12), 9.5367431640625e-07f, 4.76837158203125e-07f);
-  const float u2 = (float)(w & 0xFFFu) * 2.44140625e-04f;
-  const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u1));  // -2 ln u1
+  const float r = sqrt_approx(lgs * lg2_approx(u1));
   float sn, cs;
-  NMFA_SINCOS(6.283185307179586f * u2, sn, cs);
+  NMFA_SINCOS((float)(w & 0xFFFu) * 1.5339807878856412e-03f, sn, cs);  // 2 pi k / 4096
   z0 = r * cs;
   z1 = r * sn;
 }
+__device__ __forceinline__ float bm_scale(float sigma) { return -1.3862943611198906f * sigma * sigma; }
 
-// Eight standard normals for spins 8q..8q+7 of replica key K at step t:
+// Eight N(0, sigma^2) normals for spins 8q..8q+7 of replica key K at step t:
 // one Philox4x32-10 call, one Box-Muller pair per output word.
-__device__ __forceinline__ void normal8(const PhiloxKey& K, uint32_t q, uint32_t t, float z[8]) {
+__device__ __forceinline__ void normal8(const PhiloxKey& K, uint32_t q, uint32_t t, float lgs,
+                                        float z[8]) {
   const uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, K);
-  box_muller(w.x, z[0], z[1]);
-  box_muller(w.y, z[2], z[3]);
-  box_muller(w.z, z[4], z[5]);
-  box_muller(w.w, z[6], z[7]);
+  box_muller(w.x, lgs, z[0], z[1]);
+  box_muller(w.y, lgs, z[2], z[3]);
+  box_muller(w.z, lgs, z[4], z[5]);
+  box_muller(w.w, lgs, z[6], z[7]);
 }
 
 // The fused update of W (8 or 16) consecutive spins i0..i0+W-1 of one replica.
@@ -139,10 +144,9 @@ __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const 
 #pragma unroll
     for (int c = 0; c < W; ++c) z[c] = c < n_valid ? nz[c] : 0.f;
   } else {
+    const float lgs = bm_scale(sigma);
 #pragma unroll
-    for (int q = 0; q < W / 8; ++q) normal8(K, q0 + q, t, &z[8 * q]);
-#pragma unroll
-    for (int c = 0; c < W; ++c) z[c] *= sigma;
+    for (int q = 0; q < W / 8; ++q) normal8(K, q0 + q, t, lgs, &z[8 * q]);
   }
 #pragma unroll
   for (int q = 0; q < W / 4; ++q) {
