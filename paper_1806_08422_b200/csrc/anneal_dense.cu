@@ -433,7 +433,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     const uint32_t leader_tempty1 = map_to_rank(smem_u32(&tempty_bar[1]), 0);
     const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
     const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+    #ifdef NMFA_DBG_LOKEEP  // experiment: keep the lo residual in L2 too
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_last();
+#else
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+#endif
     int jj = 0;
     for (int ph = 0; ph < n_phases; ++ph) {
       const int t = a.t_begin + ph;
@@ -482,9 +486,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           if (valid) atomicAdd(a.energy + r, a.half_scale * e_pair + e_field);  // exact: integers
         } else {
           const bool extra = valid && (a.s_hist != nullptr || (last && a.cfg != nullptr));
+          // L1 prefetch of a chunk's state lines (no registers): the loads of chunk
+          // c + 16 are in flight while chunk c is computed
+          auto prefetch_chunk = [&](int c) {
+#ifdef NMFA_EPI_PREFETCH
+            if (c < c_hi) {
+              const long long off = img_off(tl.n0 + c);
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(a_cur + off));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.lo + off));
+              if (c + 8 < c_hi) {
+                const long long off2 = img_off(tl.n0 + c + 8);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a_cur + off2));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.lo + off2));
+              }
+            }
+#endif
+          };
           auto do_chunk = [&](auto wtag, int c) {
             constexpr int W = decltype(wtag)::value;
             const int i0 = tl.n0 + c;
+            prefetch_chunk(c + 16);
             float acc[W], ms[W], lo[W];
 #ifdef NMFA_DBG_NOTMEM  // experiment: no accumulator reads (fake fields)
 #pragma unroll
@@ -568,6 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             }
           };
           int c = c_lo;
+          prefetch_chunk(c);
           for (; c + 16 <= c_hi; c += 16) do_chunk(std::integral_constant<int, 16>{}, c);
           if (c < c_hi) do_chunk(std::integral_constant<int, 8>{}, c);
         }

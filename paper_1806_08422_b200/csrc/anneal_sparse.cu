@@ -10,6 +10,10 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef NMFA_SPARSE_MINB
+#define NMFA_SPARSE_MINB 4  // blocks per SM the register budget targets
+#endif
+
 namespace nmfa {
 
 struct SparseStepArgs {
@@ -31,53 +35,80 @@ struct SparseStepArgs {
   int last;
 };
 
-__global__ void __launch_bounds__(256) sparse_step_kernel(const SparseStepArgs a) {
+__global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(const SparseStepArgs a) {
+  // grid (replica-group blocks, spin groups): warp w of block x owns replicas
+  // [32 (8x + w), +32) of spin group y, so consecutive blocks read the same
+  // state rows (no index division; 32-bit element offsets, n * Rp < 2^31)
   const int lane = threadIdx.x & 31;
-  const long long wg = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long long nrb = a.Rp / 32;
-  const long long q = wg / nrb;
-  const long long rb = wg - q * nrb;
-  if (8 * q >= a.n) return;
-  const long long r = rb * 32 + lane;
+  const int rb = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int Rp = (int)a.Rp, n = a.n;
+  if (rb * 32 >= Rp) return;
+  const int q = blockIdx.y;
+  const int r = rb * 32 + lane;
+  const float* __restrict__ so = a.s_old + r;
+  const int* __restrict__ idx = a.idx;
+  const float* __restrict__ wts = a.w;
 
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // Memory-level parallelism: the group's 9 row pointers come from one
+  // cooperative load; then every gather of the 8 spins is issued before the
+  // first use (degree <= kFast unrolled, longer rows in a general loop).
+  constexpr int kFast = 3;  // cubic / Moebius / ladder degree; longer rows loop
+  const int i_base = 8 * q;
+  const int pl = lane <= 8 ? __ldg(a.ptr + min(i_base + lane, n)) : 0;
+  int k0[8], deg[8];
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) {
-    const int i = (int)(8 * q) + qq;
-    if (i < a.n) {
-      const int k1 = __ldg(a.ptr + i + 1);
-      float s = 0.f;
-      for (int k = __ldg(a.ptr + i); k < k1; ++k)
-        s = fmaf(__ldg(a.w + k), a.s_old[(long long)__ldg(a.idx + k) * a.Rp + r], s);
-      acc[qq] = s;
-    }
+    k0[qq] = __shfl_sync(0xffffffffu, pl, qq);
+    deg[qq] = __shfl_sync(0xffffffffu, pl, qq + 1) - k0[qq];
+  }
+  float sold[8];
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) sold[qq] = (i_base + qq < n) ? so[(i_base + qq) * Rp] : 0.f;
+  float v[8][kFast];
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+    for (int u = 0; u < kFast; ++u)
+      v[qq][u] = u < deg[qq] ? so[__ldg(idx + k0[qq] + u) * Rp] : 0.f;
+  float acc[8];
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    float s2 = 0.f;
+#pragma unroll
+    for (int u = 0; u < kFast; ++u)
+      if (u < deg[qq]) s2 = fmaf(__ldg(wts + k0[qq] + u), v[qq][u], s2);  // uniform: L1 broadcast
+    for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k)  // rows longer than kFast
+      s2 = fmaf(__ldg(wts + k), so[__ldg(idx + k) * Rp], s2);
+    acc[qq] = s2;
   }
   const bool valid = r < a.R;
   float z[8];
   if (a.noise) {
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
-      const int i = (int)(8 * q) + qq;
-      z[qq] = (valid && i < a.n) ? a.noise[((long long)r * a.t_f + a.t) * a.n + i] : 0.f;
+      const int i = i_base + qq;
+      z[qq] = (valid && i < n) ? a.noise[((long long)r * a.t_f + a.t) * n + i] : 0.f;
     }
   } else {
     const unsigned long long key = a.key_base + (unsigned long long)r;
     normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
             bm_scale(a.sigma), z);
   }
+  float* __restrict__ sn = a.s_new + r;
+  const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
+  const bool extra = valid && (a.s_hist != nullptr || a.last);
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) {
-    const int i = (int)(8 * q) + qq;
-    if (i >= a.n) break;
-    const long long o = (long long)i * a.Rp + r;
-    const float s = nmfa_update(acc[qq], __ldg(a.invn + i), __ldg(a.hn + i), z[qq], a.inv_t,
-                                a.alpha, a.oma, a.s_old[o]);
-    a.s_new[o] = s;
-    if (valid) {
-      if (a.s_hist) a.s_hist[((long long)r * a.t_f + a.t) * a.n + i] = s;
+    const int i = i_base + qq;
+    if (i >= n) break;
+    const float s = nmfa_update(acc[qq], __ldg(a.invn + i), __ldg(a.hn + i), z[qq], inv_t, alpha,
+                                oma, sold[qq]);
+    sn[i * Rp] = s;
+    if (extra) {
+      if (a.s_hist) a.s_hist[((long long)r * a.t_f + a.t) * n + i] = s;
       if (a.last) {
-        a.cfg[r * a.n + i] = s < 0.f ? (int8_t)-1 : (int8_t)1;
-        if (a.s_out) a.s_out[r * a.n + i] = s;
+        a.cfg[(long long)r * n + i] = s < 0.f ? (int8_t)-1 : (int8_t)1;
+        if (a.s_out) a.s_out[(long long)r * n + i] = s;
       }
     }
   }
@@ -118,8 +149,11 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
-  const long long warps = ((p->n + 7) / 8) * (pl->Rp / 32);
-  const unsigned blocks = (unsigned)((warps + 7) / 8);
+  if ((long long)p->n * pl->Rp >= (1LL << 31) || (p->n + 7) / 8 > 65535) {
+    set_error("sparse path: needs n <= 524280 and n x padded replicas < 2^31 per plan");
+    return NMFA_ERR_ARG;
+  }
+  const dim3 grid((unsigned)((pl->Rp / 32 + 7) / 8), (unsigned)((p->n + 7) / 8));
   float* cur = pl->d_sa;
   float* nxt = pl->d_sb;
   for (int t = 0; t < pl->t_f; ++t) {
@@ -128,7 +162,7 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
     a.last = (t == pl->t_f - 1);
     a.s_old = cur;
     a.s_new = nxt;
-    sparse_step_kernel<<<blocks, 256, 0, st>>>(a);
+    sparse_step_kernel<<<grid, 256, 0, st>>>(a);
     NMFA_LAUNCH_CHECK();
     std::swap(cur, nxt);
   }
