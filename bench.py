@@ -9,7 +9,7 @@ sharded with no data-path collective; one all-gather of each rank's best at
 the end).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload k2000|sk100|moebius100|g2000|sk65536]
+                    [--workload k2000|sk100|moebius100|g2000|moebius131072|sk65536]
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle port
 of the reference's per-run loop (oracle/nmfa_oracle.py, which follows
@@ -38,11 +38,19 @@ WORKLOADS = {
                    "Moebius ladder n=100, 37888 reads/GPU, t_f=1000"),
     "g2000": ("gen_dense_maxcut(2000, 0.01, 7)", 2000, 4096, 1000,
               "G-set-style gen_dense_maxcut(2000,0.01,7), 4096 reads/GPU, t_f=1000"),
+    # the CSR path where it is the routed one (large, low-degree sparse instance)
+    "moebius131072": ("moebius_ladder(131072)", 131072, 1024, 200,
+                      "Moebius ladder n=131072 (CSR path), 1024 reads/GPU, t_f=200"),
     # config 5: J generated on device, row-sharded over the ranks (strong scaling)
     "sk65536": (None, 65536, 1024, 200,
                 "synthetic SK N=65536 (on-device Philox J, seed 7), 1024 reads total, t_f=200, "
                 "J row-sharded, S all-gathered each sweep"),
 }
+
+
+def metric_name(workload):
+    return ("spin-updates/s (N*reads*steps/s) on K2000" if workload == "k2000"
+            else f"spin-updates/s (N*reads*steps/s) on {workload}")
 
 
 def build_problem(nb, name):
@@ -143,7 +151,8 @@ def cpu_reference(workload, sample_runs=None, threads=None):
     op = O.problem_from_edges(p.n, p.edges_i, p.edges_j, p.edge_weights, p.h)
     threads = threads or os.cpu_count() or 1
     if sample_runs is None:
-        sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads}.get(workload, 64 * threads)
+        sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads,
+                       "moebius131072": threads}.get(workload, 64 * threads)
     O.batch(op, 10**6, threads, t_f=20, threads=threads)  # warm BLAS / thread pool
     t0 = time.perf_counter()
     _, e = O.batch(op, 0, sample_runs, t_f=t_f, threads=threads)
@@ -223,7 +232,7 @@ def run_reference(args):
             steps.append(r)
             cb = r
     value = statistics.median(s["value"] for s in steps)
-    line = {"metric": "spin-updates/s (N*reads*steps/s) on K2000", "value": value,
+    line = {"metric": metric_name(args.workload), "value": value,
             "unit": "spin-updates/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(s["wall_s"] for s in steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -364,18 +373,22 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     launches = 0
+    # L2 is flushed between timed steps (a 256 MB write, outside the per-step
+    # CUDA-event brackets), so no step starts with the previous step's J/state hot
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
-        ev0.record(stream)
         for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            evs[k][0].record(stream)
             launches += step(args.warmup + k)
-        ev1.record(stream)
+            evs[k][1].record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -456,15 +469,16 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": "spin-updates/s (N*reads*steps/s) on K2000", "value": value,
+            "metric": metric_name(args.workload), "value": value,
             "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f16 operand / f32 state",
-            "data": "synthetic (reference generator stream, gen_sk(2000,7))",
+            "data": f"synthetic (reference generator stream, {WORKLOADS[args.workload][0]})",
             "config": {"workload": desc, "reads_per_gpu": R, "reads_total": R * world,
                        "n": n, "t_f": t_f, "path": info["path"],
                        "parallelism": f"replica-sharded x{world}",
-                       "l2": "state (>=100 MB per GPU at K2000) exceeds L2; no flush needed",
+                       "l2": "flushed between timed steps (256 MB write outside the per-step "
+                             "event brackets); value = steps x work / sum of step times",
                        "best_energy": float(gbest[0]), "best_replica": int(gbest[1])},
             "roofline": roof,
             "cpu_baseline": cpu_bl,

@@ -1,4 +1,4 @@
-"""Short runs of each kernel path for ncu captures: small (SK100), sparse (G2000), dense (K2000)."""
+"""Short runs of each kernel path for ncu captures: small (SK100), sparse (Moebius 131072), dense (K2000)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -7,7 +7,7 @@ which = sys.argv[1]
 if which == "small":
     p, R, t_f = nb.gen_sk(100, 0), 37888, 1000
 elif which == "sparse":
-    p, R, t_f = nb.gen_dense_maxcut(2000, 0.01, 7), 4096, 8
+    p, R, t_f = nb.moebius_ladder(131072), 1024, 8
 else:
     p, R, t_f = nb.gen_sk(2000, 7), 8192, int(os.environ.get("PROF_TF", "3"))
 params = nb.NmfaParams(t_f=t_f, seed=0)
