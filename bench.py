@@ -9,7 +9,7 @@ sharded with no data-path collective; one all-gather of each rank's best at
 the end).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload k2000|sk100|moebius100|g2000|moebius131072|sk65536]
+                    [--workload k2000|sk100|moebius100|g2000|moebius131072|ground26|sk65536]
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle port
 of the reference's per-run loop (oracle/nmfa_oracle.py, which follows
@@ -41,6 +41,8 @@ WORKLOADS = {
     # the CSR path where it is the routed one (large, low-degree sparse instance)
     "moebius131072": ("moebius_ladder(131072)", 131072, 1024, 200,
                       "Moebius ladder n=131072 (CSR path), 1024 reads/GPU, t_f=200"),
+    # exhaustive ground state (brute_force_ground) at the reference's limit
+    "ground26": ("gen_sk(26, 1)", 26, 1, 1, "exact ground state of gen_sk(26,1) by Gray-code enumeration"),
     # config 5: J generated on device, row-sharded over the ranks (strong scaling)
     "sk65536": (None, 65536, 1024, 200,
                 "synthetic SK N=65536 (on-device Philox J, seed 7), 1024 reads total, t_f=200, "
@@ -333,6 +335,80 @@ def run_sk65536(args):
         dist.destroy_process_group()
 
 
+def run_ground(args, impl):
+    """brute_force_ground on gen_sk(26, 1): one step = one full enumeration of
+    2^26 configurations; metric configurations/s.  The reference arm times the
+    oracle's numba restatement of the reference's sequential Gray walk
+    (_kernels_numba.py:83-114) on one host core (the reference is sequential)."""
+    import numpy as np
+
+    import paper_1806_08422_b200 as nb
+
+    world, rank, _ = dist_init()
+    p = nb.gen_sk(26, 1)
+    n = p.n
+    desc = WORKLOADS["ground26"][4]
+    if impl == "reference":
+        if rank == 0:
+            sys.path.insert(0, os.path.join(REPO, "oracle"))
+            import nmfa_oracle as O
+            op = O.problem_from_edges(n, p.edges_i, p.edges_j, p.edge_weights)
+            O.gray_ground_fast(O.problem_from_edges(4, [0], [1], [1.0]))  # jit
+            times = []
+            for _ in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                e, c = O.gray_ground_fast(op)
+                times.append(time.perf_counter() - t0)
+            dt = statistics.median(times[args.warmup:])
+            v = 2.0 ** n / dt
+            print(json.dumps({
+                "metric": "configurations/s (2^n / enumeration time), exact ground state", "value": v,
+                "unit": "configurations/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference", "config": {"workload": desc, "energy": e, "degeneracy": c},
+                "cpu_baseline": {"value": v, "unit": "configurations/s", "cores": 1, "kind": "port",
+                                 "sample": "full 2^26 enumeration"},
+                "e2e": {"value": v, "unit": "configurations/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    import torch
+    nb.brute_force_ground(p)  # warm-up: builds the device problem
+    with ClockSampler(0) as clk:
+        times = []
+        for _ in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            gt = nb.brute_force_ground(p)   # synchronous host API (host in, host out)
+            times.append(time.perf_counter() - t0)
+    dt = statistics.median(times[args.warmup:])
+    value = 2.0 ** n / dt
+    cpu_bl = None
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import nmfa_oracle as O
+        op = O.problem_from_edges(n, p.edges_i, p.edges_j, p.edge_weights)
+        O.gray_ground_fast(O.problem_from_edges(4, [0], [1], [1.0]))
+        t0 = time.perf_counter()
+        O.gray_ground_fast(op)
+        cdt = time.perf_counter() - t0
+        cpu_bl = {"value": 2.0 ** n / cdt, "unit": "configurations/s", "cores": 1, "kind": "port",
+                  "sample": "full 2^26 enumeration (numba restatement of gray_ground)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "configurations/s (2^n / enumeration time), exact ground state", "value": value,
+            "unit": "configurations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64 (popcount fields)", "data": "synthetic",
+            "config": {"workload": desc, "n": n, "energy": gt.energy, "degeneracy": gt.degeneracy,
+                       "timing": "host wall clock around the synchronous C-ABI call"},
+            "roofline": None,
+            "cpu_baseline": cpu_bl,
+            "e2e": {"value": value, "unit": "configurations/s", "h2d_bytes_per_step": n * n * 8 + n * 40,
+                    "d2h_bytes_per_step": 24 * max(1, (1 << (n - 1 - 9)) // 256),
+                    "api": "brute_force_ground -> nmfa_ground_state (C ABI, host buffers)"},
+            "gpu_launches": 1, "clocks": clk.summary()}), flush=True)
+
+
 def run_ours(args):
     import ctypes
 
@@ -509,6 +585,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the SK100 TTS99 side measurement")
     args = ap.parse_args()
+    if args.workload == "ground26":
+        run_ground(args, args.impl)
+        return
     if args.workload == "sk65536":
         if args.impl == "reference":
             if int(os.environ.get("RANK", "0")) == 0:

@@ -150,6 +150,16 @@ int nmfa_energy(const nmfa_problem_t* p, const int8_t* config_dev, int64_t n_con
 int nmfa_best_of(const double* energy_dev, int64_t n, double* best_energy_dev,
                  int64_t* best_index_dev, void* stream);
 
+/* Exact ground state by exhaustive enumeration: minimum energy over all 2^n
+ * configurations and its degeneracy (brute_force_ground, metrics.py:53-67;
+ * gray_ground, _kernels_numba.py:83-114: Gray-code single-flip walk, ties
+ * within 1e-9).  Exact integer arithmetic when every coupler is in {-1,0,+1}
+ * and h is integer, else float64.  NMFA_ERR_ARG if n > max_n (the reference's
+ * MAX_EXACT_N = 26; this implementation allows up to 40).  config_host, if not
+ * NULL, receives one minimising configuration (+-1).  Synchronous. */
+int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy_host,
+                      int64_t* degeneracy_host, int8_t* config_host);
+
 const char* nmfa_last_error(void);
 const char* nmfa_version(void);
 /* Number of kernels the last nmfa_plan_run on this thread enqueued. */

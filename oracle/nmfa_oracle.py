@@ -341,3 +341,79 @@ def sk_device_couplings(n, seed):
     J = np.zeros((n, n))
     J[i, j] = np.where(bit == 1, 1.0, -1.0)
     return J + J.T
+
+
+# --------------------------------------------------------------------------
+# Exact ground state (brute_force_ground, metrics.py:53-67).  Restates the
+# reference's chunked numpy enumerator (_kernels_numpy.py:64-87): energies of
+# every configuration k (bit i of k set -> s_i = -1, as 1 - 2*bits), minimum
+# and the count within TIE_TOL.  Test infrastructure; the product enumerates
+# on the GPU (csrc/ground.cu).
+# --------------------------------------------------------------------------
+TIE_TOL = 1e-9
+
+
+def gray_ground(problem, chunk_bits=16):
+    n = problem.n
+    J = np.zeros((n, n))
+    J[problem.edges_i, problem.edges_j] = problem.edge_weights
+    J = J + J.T
+    h = np.asarray(problem.h, dtype=np.float64)
+    shifts = np.arange(n, dtype=np.uint64)
+    total = 1 << n
+    chunk = min(total, 1 << chunk_bits)
+    emin, count = np.inf, 0
+    for start in range(0, total, chunk):
+        ks = np.arange(start, min(start + chunk, total), dtype=np.uint64)
+        S = 1.0 - 2.0 * ((ks[:, None] >> shifts[None, :]) & np.uint64(1))
+        E = 0.5 * np.einsum("bi,bi->b", S @ J, S) + S @ h
+        cmin = float(E.min())
+        if cmin < emin - TIE_TOL:
+            emin = cmin
+            count = int(np.count_nonzero(E <= emin + TIE_TOL))
+        else:
+            count += int(np.count_nonzero(E <= emin + TIE_TOL))
+    return emin, count
+
+
+def gray_ground_fast(problem):
+    """numba restatement of the reference's sequential Gray walk
+    (_kernels_numba.py:83-114): the CPU baseline for the enumerator."""
+    from numba import njit
+
+    global _gray_jit
+    if "_gray_jit" not in globals():
+        @njit(cache=False, nogil=True)
+        def _gray(indptr, indices, weights, h):
+            n = h.shape[0]
+            s = np.full(n, -1.0)
+            e = 0.0
+            for i in range(n):
+                for k in range(indptr[i], indptr[i + 1]):
+                    j = indices[k]
+                    if j > i:
+                        e += weights[k] * s[i] * s[j]
+                e += h[i] * s[i]
+            emin = e
+            count = 1
+            total = np.int64(1) << n
+            for step in range(1, total):
+                v = 0
+                k = step
+                while k & 1 == 0:
+                    k >>= 1
+                    v += 1
+                s[v] = -s[v]
+                acc = 0.0
+                for k in range(indptr[v], indptr[v + 1]):
+                    acc += weights[k] * s[indices[k]]
+                e += 2.0 * s[v] * (h[v] + acc)
+                if e < emin - 1e-9:
+                    emin = e
+                    count = 1
+                elif e <= emin + 1e-9:
+                    count += 1
+            return emin, count
+        _gray_jit = _gray
+    return _gray_jit(problem.csr_indptr, problem.csr_indices, problem.csr_weights,
+                     np.asarray(problem.h, dtype=np.float64))

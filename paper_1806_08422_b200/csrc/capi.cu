@@ -536,6 +536,18 @@ int nmfa_plan_run_sweeps(nmfa_plan_t* pl, uint64_t seed, int64_t r0, int32_t t_b
   return err;
 }
 
+int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy,
+                      int64_t* degeneracy, int8_t* config) {
+  if (!p || !energy || !degeneracy) return arg_error("NULL argument");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  g_launches = 0;
+  const int err = ground_state(p, max_n, energy, degeneracy, config);
+  cudaSetDevice(prev);
+  return err;
+}
+
 int nmfa_plan_image_info(const nmfa_plan_t* pl, void** img0, void** img1, int64_t* slice_bytes,
                          int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi) {
   if (!pl || !img0 || !img1 || !slice_bytes || !n_slices || !slice_lo || !slice_hi)

@@ -116,6 +116,8 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         double* energy, bool* energy_done, cudaStream_t st);
 bool dense_energy_exact(const nmfa_problem* p);
+int ground_state(const nmfa_problem* p, int max_n, double* energy, int64_t* degeneracy,
+                 int8_t* config);
 bool dense_is_sharded(const nmfa_problem* p);
 int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise, const float* s0,
                      int8_t* cfg, float* s_out, float* s_hist, double* energy, int t_begin,
