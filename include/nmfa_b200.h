@@ -133,6 +133,18 @@ int nmfa_anneal(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,
                 double* energy_dev, float* s_final_dev, float* s_hist_dev,
                 double* e_hist_dev, void* stream);
 
+/* Many instances, one call (the Fig. 4-style sweep of cli.py:280-347, where
+ * the reference runs nmfa_batch once per instance).  Instance k runs n_reads
+ * replicas with keys seeds[k] + r (its nmfa_batch seed, cli.py:319-321);
+ * config_dev [count][n_reads][n] i8, energy_dev [count][n_reads] f64 (or NULL).
+ * Every instance must have the same n.  Small instances (n <= 256) run in ONE
+ * persistent launch (grid = replica blocks x instances); larger ones fall back
+ * to one anneal per instance.  Synchronous on `stream`. */
+int nmfa_anneal_many(const nmfa_problem_t* const* problems, int32_t count, int64_t n_reads,
+                     int32_t t_f, const double* temps_host, double alpha, double sigma,
+                     const uint64_t* seeds_host, int8_t* config_dev, double* energy_dev,
+                     void* stream);
+
 /* Same batch with HOST buffers (H2D of inputs, D2H of results inside the
  * call; synchronous).  This is the end-to-end entry a non-CUDA host binds. */
 int nmfa_anneal_host(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,

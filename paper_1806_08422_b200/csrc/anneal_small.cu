@@ -9,13 +9,25 @@
 // fused update (reference _kernels_numba.py:71-75) and writes the new fp16
 // operand back into SMEM.  No HBM traffic inside the anneal.
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
 
 namespace nmfa {
 
+// One instance of a grouped launch (nmfa_anneal_many): every instance has the
+// same padded size np and replica count R; blockIdx.y selects the instance.
+struct SmallInstance {
+  const uint4* j_img;
+  const float* invn;
+  const float* hn;
+  unsigned long long key_base;
+  int8_t* cfg;  // [R][n]
+};
+
 struct SmallArgs {
+  const SmallInstance* inst;  // grouped launch table, or null (single problem below)
   const uint4* j_img;
   uint32_t j_bytes;
   const float* invn;
@@ -52,9 +64,14 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
   const long long rrel = (long long)blockIdx.x * kRowsPerCta + rl;
   const bool valid = rrel < a.R;
   const int nchunks = np / 16;
+  const SmallInstance* I = a.inst ? a.inst + blockIdx.y : nullptr;
+  const uint4* j_img = I ? I->j_img : a.j_img;
+  const float* invn = I ? I->invn : a.invn;
+  const float* hn = I ? I->hn : a.hn;
+  int8_t* cfg = I ? I->cfg : a.cfg;
 
   for (uint32_t i = tid; i < a.j_bytes / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(sJ)[i] = a.j_img[i];
+    reinterpret_cast<uint4*>(sJ)[i] = j_img[i];
   if (warp == 0) tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -67,7 +84,7 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
   const uint32_t t_acc = tbase + ((uint32_t)(32 * quarter) << 16);
   const uint32_t t_mst = t_acc + (uint32_t)np;
 
-  const unsigned long long key = a.key_base + (unsigned long long)rrel;
+  const unsigned long long key = (I ? I->key_base : a.key_base) + (unsigned long long)rrel;
   const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
 
   // initial state: s0 or zeros, into the TMEM master and the SMEM operand
@@ -111,8 +128,8 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
     const float inv_t = a.inv_temp[t];
     const bool last = (t == a.t_f - 1);
 
-    const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
-    const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
+    const float4* invn4 = reinterpret_cast<const float4*>(invn);
+    const float4* hn4 = reinterpret_cast<const float4*>(hn);
     const bool extra = (a.s_hist != nullptr) || last;
     for (int j = cpart; j < nchunks; j += a.cs) {
       const int c0 = 16 * j;
@@ -142,7 +159,7 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             if (c < nvalid) {
-              a.cfg[rrel * a.n + c0 + c] = ms[c] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181-183
+              cfg[rrel * a.n + c0 + c] = ms[c] < 0.f ? (int8_t)-1 : (int8_t)1;  // problem.py:181-183
               if (a.s_out) a.s_out[rrel * a.n + c0 + c] = ms[c];
             }
           }
@@ -203,6 +220,52 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   kern<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
   NMFA_LAUNCH_CHECK();
   add_launches(1);
+  return NMFA_OK;
+}
+
+// Grouped launch: `count` small problems of the same padded size, R replicas
+// each, in ONE persistent launch (grid = CTAs per instance x count), so many
+// small instances fill the GPU (Fig. 4-style sweeps, cli.py:280-347).
+int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R, int t_f,
+                             const float* d_inv_temp, float alpha, float sigma,
+                             const uint64_t* key_bases, int8_t* cfg, cudaStream_t st) {
+  const nmfa_problem* p0 = ps[0];
+  std::vector<SmallInstance> h(count);
+  for (int k = 0; k < count; ++k) {
+    h[k].j_img = reinterpret_cast<const uint4*>(ps[k]->d_j_small);
+    h[k].invn = ps[k]->d_invn;
+    h[k].hn = ps[k]->d_hn;
+    h[k].key_base = key_bases[k];
+    h[k].cfg = cfg + (size_t)k * R * p0->n;
+  }
+  SmallInstance* d_inst = nullptr;
+  NMFA_CUDA_TRY(cudaMallocAsync(&d_inst, sizeof(SmallInstance) * count, st));
+  NMFA_CUDA_TRY(cudaMemcpyAsync(d_inst, h.data(), sizeof(SmallInstance) * count,
+                                cudaMemcpyHostToDevice, st));
+  SmallArgs a{};
+  a.inst = d_inst;
+  a.j_bytes = (uint32_t)p0->np * p0->np * 2;
+  a.inv_temp = d_inv_temp;
+  a.n = (int)p0->n;
+  a.np = p0->np;
+  a.t_f = t_f;
+  a.tmem_cols = pow2_cols(2u * p0->np);
+  a.alpha = alpha;
+  a.oma = 1.0f - alpha;
+  a.sigma = sigma;
+  a.R = R;
+  const long long ctas = (R + kRowsPerCta - 1) / kRowsPerCta;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p0->device);
+  a.cs = ctas * count >= sms ? 2 : 4;
+  if (a.cs > p0->np / 16) a.cs = p0->np / 16;
+  const size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 + 16;
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(small_anneal_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  small_anneal_kernel<false><<<dim3((unsigned)ctas, (unsigned)count), 128 * a.cs, smem, st>>>(a);
+  NMFA_LAUNCH_CHECK();
+  add_launches(1);
+  NMFA_CUDA_TRY(cudaFreeAsync(d_inst, st));
   return NMFA_OK;
 }
 

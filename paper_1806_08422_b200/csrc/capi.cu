@@ -601,6 +601,82 @@ int nmfa_anneal(const nmfa_problem_t* cp, int64_t R, int32_t t_f, const double* 
   return err;
 }
 
+int nmfa_anneal_many(const nmfa_problem_t* const* ps, int32_t count, int64_t R, int32_t t_f,
+                     const double* temps, double alpha, double sigma, const uint64_t* seeds,
+                     int8_t* cfg, double* energy, void* stream) {
+  if (!ps || !seeds || !cfg || count < 1) return arg_error("NULL argument or empty instance list");
+  if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
+  if (!temps || t_f < 1) return arg_error("t_f must be at least 1, got " + std::to_string(t_f));
+  if (!(alpha >= 0.0 && alpha <= 1.0))
+    return arg_error("alpha must be in [0, 1], got " + std::to_string(alpha));
+  if (!(sigma >= 0.0)) return arg_error("sigma must be nonnegative, got " + std::to_string(sigma));
+  const int64_t n = ps[0] ? ps[0]->n : 0;
+  bool grouped = true;
+  for (int32_t k = 0; k < count; ++k) {
+    if (!ps[k]) return arg_error("NULL problem in the instance list");
+    if (ps[k]->n != n) return arg_error("every instance of a group must have the same n");
+    if (ps[k]->device != ps[0]->device) return arg_error("instances must live on one device");
+    grouped = grouped && ps[k]->path == NMFA_PATH_SMALL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!grouped) {  // larger instances: one (cached-plan) anneal per instance
+    for (int32_t k = 0; k < count; ++k) {
+      const int err = nmfa_anneal(ps[k], R, t_f, temps, alpha, sigma, seeds[k], 0, nullptr,
+                                  nullptr, cfg + (size_t)k * R * n,
+                                  energy ? energy + (size_t)k * R : nullptr, nullptr, nullptr,
+                                  nullptr, stream);
+      if (err) return err;
+    }
+    return NMFA_OK;
+  }
+  std::vector<float> inv_t(t_f);
+  for (int32_t t = 0; t < t_f; ++t) {
+    if (!(temps[t] > 0.0) || !std::isfinite(temps[t]))
+      return arg_error("temperature must be positive, got " + std::to_string(temps[t]));
+    inv_t[t] = (float)(1.0 / temps[t]);
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ps[0]->device);
+  g_launches = 0;
+  int err = NMFA_OK;
+  float* d_inv = nullptr;
+  uint32_t* bits = nullptr;
+  double* part = nullptr;
+  do {
+    if (cudaMallocAsync(&d_inv, 4 * t_f, st) != cudaSuccess ||
+        cudaMemcpyAsync(d_inv, inv_t.data(), 4 * t_f, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      set_error("out of device memory for the schedule");
+      err = NMFA_ERR_CUDA;
+      break;
+    }
+    std::vector<uint64_t> keys(seeds, seeds + count);
+    err = launch_small_anneal_many(ps, count, R, t_f, d_inv, (float)alpha, (float)sigma,
+                                   keys.data(), cfg, st);
+    if (err || !energy) break;
+    int64_t chunks = 1;
+    for (int32_t k = 0; k < count; ++k) chunks = std::max(chunks, energy_chunks_for(ps[k], R));
+    if (cudaMallocAsync(&bits, (size_t)n * ((R + 31) / 32) * 4, st) != cudaSuccess ||
+        cudaMallocAsync(&part, (size_t)(chunks + 1) * R * 8, st) != cudaSuccess) {
+      set_error("out of device memory for energy scratch");
+      err = NMFA_ERR_CUDA;
+      break;
+    }
+    for (int32_t k = 0; k < count && !err; ++k)
+      err = launch_energy(ps[k], cfg + (size_t)k * R * n, R, energy + (size_t)k * R, bits, part,
+                          energy_chunks_for(ps[k], R), st);
+  } while (0);
+  if (d_inv) cudaFreeAsync(d_inv, st);
+  if (bits) cudaFreeAsync(bits, st);
+  if (part) cudaFreeAsync(part, st);
+  if (!err && cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error(std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
+    err = NMFA_ERR_CUDA;
+  }
+  cudaSetDevice(prev);
+  return err;
+}
+
 int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
                      double alpha, double sigma, uint64_t seed, int64_t r0, int8_t* cfg_host,
                      double* energy_host) {

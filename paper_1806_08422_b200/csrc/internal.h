@@ -116,6 +116,9 @@ int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         double* energy, bool* energy_done, cudaStream_t st);
 bool dense_energy_exact(const nmfa_problem* p);
+int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R, int t_f,
+                             const float* d_inv_temp, float alpha, float sigma,
+                             const uint64_t* key_bases, int8_t* cfg, cudaStream_t st);
 int ground_state(const nmfa_problem* p, int max_n, double* energy, int64_t* degeneracy,
                  int8_t* config);
 bool dense_is_sharded(const nmfa_problem* p);

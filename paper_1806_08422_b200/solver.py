@@ -296,6 +296,50 @@ def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=Non
 # ---------------------------------------------------------------------------
 # reference-compatible entry points
 # ---------------------------------------------------------------------------
+def sample_many(problems, params=None, n_runs=1, *, seeds=None, device=0):
+    """Anneal many instances of the same size in one call (nmfa_anneal_many).
+
+    Instance k runs ``n_runs`` replicas seeded like the reference's bench loop
+    (cli.py:319-321): ``seeds[k]`` defaults to ``params.seed + k * n_runs``, and
+    replica r uses key ``seeds[k] + r`` -- identical to ``sample(problems[k],
+    replace(params, seed=seeds[k]), n_runs)``.  Small instances (n <= 256) share
+    ONE persistent launch.  Returns (configs int8 (K, R, n), energies f64 (K, R))
+    as device tensors and the wall time of the whole call.
+    """
+    import ctypes
+
+    import torch
+
+    params = NmfaParams() if params is None else params
+    probs = [as_problem(p) for p in problems]
+    if not probs:
+        raise ValueError("sample_many needs at least one instance")
+    n = probs[0].n
+    if any(p.n != n for p in probs):
+        raise ValueError("every instance of a group must have the same n")
+    n_runs = int(n_runs)
+    if n_runs < 1:
+        raise ValueError(f"n_runs must be at least 1, got {n_runs}")
+    K = len(probs)
+    if seeds is None:
+        seeds = [(int(params.seed) + k * n_runs) & MASK64 for k in range(K)]
+    seeds = np.ascontiguousarray([int(x) & MASK64 for x in seeds], dtype=np.uint64)
+    if seeds.size != K:
+        raise ValueError("seeds must have one entry per instance")
+    temps = np.ascontiguousarray(params.schedule.temperatures(params.t_f), dtype=np.float64)
+    handles = (ctypes.c_void_p * K)(*[p.device_handle(device).handle.value for p in probs])
+    dev = torch.device("cuda", device)
+    cfg = torch.empty((K, n_runs, n), dtype=torch.int8, device=dev)
+    en = torch.empty((K, n_runs), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    _native.check(_native.load().nmfa_anneal_many(
+        ctypes.cast(handles, ctypes.c_void_p), K, n_runs, int(params.t_f), _native.ptr(temps),
+        float(params.alpha), float(params.sigma), _native.ptr(seeds), _native.ptr(cfg),
+        _native.ptr(en), ctypes.c_void_p(stream.cuda_stream)))
+    return cfg, en, time.perf_counter() - t0
+
+
 def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=False, device=0):
     """Anneal with caller-supplied, pre-scaled noise (solver.py:188-218).
 
