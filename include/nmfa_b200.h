@@ -162,6 +162,14 @@ int nmfa_energy(const nmfa_problem_t* p, const int8_t* config_dev, int64_t n_con
 int nmfa_best_of(const double* energy_dev, int64_t n, double* best_energy_dev,
                  int64_t* best_index_dev, void* stream);
 
+/* Parse edge-list / G-set instance text (parse_gset, gset.py:35-89): header
+ * "n m", then m lines "u v w" (1-based), '#'/'c' comment lines.  Call once
+ * with edges_i == NULL to read n and m, then with arrays of capacity >= m to
+ * receive the 0-based edges in file order.  Errors follow the reference
+ * (GsetParseError): NMFA_ERR_ARG with "line N: <message>" in nmfa_last_error. */
+int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out,
+                    int64_t* edges_i, int64_t* edges_j, double* weights, int64_t cap);
+
 /* Exact ground state by exhaustive enumeration: minimum energy over all 2^n
  * configurations and its degeneracy (brute_force_ground, metrics.py:53-67;
  * gray_ground, _kernels_numba.py:83-114: Gray-code single-flip walk, ties

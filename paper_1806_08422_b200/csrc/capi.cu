@@ -536,6 +536,14 @@ int nmfa_plan_run_sweeps(nmfa_plan_t* pl, uint64_t seed, int64_t r0, int32_t t_b
   return err;
 }
 
+int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out,
+                    int64_t* edges_i, int64_t* edges_j, double* weights, int64_t cap) {
+  if (!text || len < 0 || !n_out || !m_out) return arg_error("NULL argument");
+  if ((edges_i || edges_j || weights) && !(edges_i && edges_j && weights))
+    return arg_error("edge arrays must be all NULL (header query) or all set");
+  return gset_parse(text, len, n_out, m_out, edges_i, edges_j, weights, cap);
+}
+
 int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy,
                       int64_t* degeneracy, int8_t* config) {
   if (!p || !energy || !degeneracy) return arg_error("NULL argument");

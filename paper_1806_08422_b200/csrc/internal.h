@@ -119,6 +119,8 @@ bool dense_energy_exact(const nmfa_problem* p);
 int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R, int t_f,
                              const float* d_inv_temp, float alpha, float sigma,
                              const uint64_t* key_bases, int8_t* cfg, cudaStream_t st);
+int gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out, int64_t* ei,
+               int64_t* ej, double* w, int64_t cap);
 int ground_state(const nmfa_problem* p, int max_n, double* energy, int64_t* degeneracy,
                  int8_t* config);
 bool dense_is_sharded(const nmfa_problem* p);
