@@ -827,7 +827,15 @@ int dense_plan_alloc(nmfa_plan* pl) {
   std::vector<DenseTile> tiles;
   tiles.reserve(T);
   std::vector<int> off(pairs + 1, 0);
-  if (order == "spin") {
+  if (order == "block") {
+    // m-major list dealt round-robin: at position j the pairs hold whole replica
+    // blocks (~pairs / tiles-per-block of them), so block m's sweep-t tiles all
+    // finish at one position and its sweep-(t+1) tiles run a full sweep later
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int)tiles.size();
+      for (long long j = q; j < T; j += pairs) tiles.push_back(mmaj[j]);
+    }
+  } else if (order == "spin") {
     std::vector<DenseTile> sorted(mmaj);
     std::stable_sort(sorted.begin(), sorted.end(),
                      [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
