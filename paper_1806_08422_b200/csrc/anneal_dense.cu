@@ -851,6 +851,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
       if (order == "sorted")
         std::stable_sort(run.begin(), run.end(),
                          [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
+      if ((order == "alt" && (q & 1)) || order == "rev") std::reverse(run.begin(), run.end());
       tiles.insert(tiles.end(), run.begin(), run.end());
     }
   }
