@@ -139,8 +139,12 @@ __global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a)
       tmem_wait_ld();
       const int nvalid = valid ? min(16, a.n - c0) : 0;
       const float* nz = kInjected ? a.noise + ((long long)rrel * a.t_f + t) * a.n + c0 : nullptr;
-      update16<kInjected>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
-                          (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+      if (a.n - c0 <= 8)  // the padded tail chunk: columns >= n only meet zero J columns
+        update_chunk<kInjected, 8>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
+                                   (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+      else
+        update16<kInjected>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
+                            (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
       tmem_st16(t_mst + c0, ms);
       uint4 lo = make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
                             pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
