@@ -80,7 +80,10 @@ int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int6
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path);
 
 /* A plan owns the device state for `n_reads` replicas and `t_f` steps so
- * repeated runs allocate nothing and can be captured in a CUDA graph.
+ * repeated runs allocate nothing and can be captured in a CUDA graph.  A plan
+ * runs one batch at a time (use one plan per concurrent stream); problems are
+ * immutable and shareable, and nmfa_anneal / nmfa_anneal_host serialise their
+ * per-problem caches internally.
  * temps_host: t_f temperatures (Schedule.temperatures, solver.py:70-84),
  * each > 0.  alpha in [0,1], sigma >= 0 (NmfaParams, solver.py:141-162). */
 int nmfa_plan_create(const nmfa_problem_t* p, int64_t n_reads, int32_t t_f,

@@ -698,6 +698,9 @@ int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   auto* mp = const_cast<nmfa_problem*>(p);
+  // the cached stream and result buffers are shared by every host-entry call
+  // on this problem: hold them for the whole call
+  std::lock_guard<std::mutex> host_lock(mp->host_mu);
   int err = NMFA_OK;
   {
     // device result buffers and the stream are cached on the problem handle

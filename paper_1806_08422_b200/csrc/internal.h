@@ -73,6 +73,7 @@ struct nmfa_problem {
   // one-shot entry points (nmfa_anneal / nmfa_anneal_host) reuse one cached
   // plan; the mutex serialises them (they are synchronous).
   std::mutex cache_mu;
+  std::mutex host_mu;  // serialises nmfa_anneal_host calls (they share the cached buffers)
   nmfa_plan* cached_plan = nullptr;
   std::vector<double> cached_temps;
   double cached_alpha = -1.0, cached_sigma = -1.0;

@@ -332,3 +332,39 @@ def test_k2000_standin_energy_distribution(G):
     print(f"k2000 mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
           f"min_ref={ref.min()} se={se:.2f}")
     assert abs(e.mean() - ref.mean()) < 4 * se
+
+
+def test_host_entry_is_thread_safe():
+    """Concurrent nmfa_anneal_host calls on one problem (different read counts,
+    so the cached buffers are resized) give the same results as sequential ones."""
+    import ctypes
+    import threading
+
+    from paper_1806_08422_b200 import _native
+    p = nb.gen_sk(120, 4)
+    params = nb.NmfaParams(t_f=100, seed=9)
+    temps = np.ascontiguousarray(params.schedule.temperatures(params.t_f))
+    lib = _native.load()
+    h = p.device_handle().handle
+
+    def call(R, seed):
+        cfg = np.empty((R, p.n), np.int8)
+        e = np.empty(R)
+        _native.check(lib.nmfa_anneal_host(h, R, params.t_f, _native.ptr(temps), params.alpha,
+                                           params.sigma, seed, 0, _native.ptr(cfg), _native.ptr(e)))
+        return cfg, e
+
+    jobs = [(256 + 128 * (k % 3), 100 + k) for k in range(8)]
+    want = [call(R, s) for R, s in jobs]
+    got = [None] * len(jobs)
+
+    def worker(k):
+        got[k] = call(*jobs[k])
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(len(jobs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for (wc, we), (gc, ge) in zip(want, got):
+        assert np.array_equal(wc, gc) and np.array_equal(we, ge)
