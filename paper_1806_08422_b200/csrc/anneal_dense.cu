@@ -461,8 +461,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         // this warp's columns: a contiguous, 8-aligned quarter of the tile (balanced to 8 spins)
         const int n8 = tl.nlen >> 3;
         const int c_lo = (n8 * hpart / kParts) * 8, c_hi = (n8 * (hpart + 1) / kParts) * 8;
+        // byte offset of spins i..i+7 of replica r in an operand image: 32-bit
+        // (plans keep each image below 4 GiB), k-slice stride Rp * 256 bytes
+        const uint32_t slice_bytes = (uint32_t)a.Rp * 256u, row_off32 = (uint32_t)row_off;
         auto img_off = [&](int i) {
-          return (long long)(i >> 7) * a.Rp * 256 + row_off + ((i & 127) >> 3) * 128;
+          return (uint32_t)(i >> 7) * slice_bytes + row_off32 + (uint32_t)((i & 127) >> 3) * 128u;
         };
         if (energy_phase) {
           // a_cur holds the +-1 configuration written by the last sweep
@@ -524,7 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
 #endif
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
-              const long long off = img_off(i0 + 8 * h);
+              const uint32_t off = img_off(i0 + 8 * h);
 #if defined(NMFA_DBG_NOLOAD)
 #pragma unroll
               for (int q = 0; q < 8; ++q) { ms[8 * h + q] = 0.01f * q; lo[8 * h + q] = 0.f; }
@@ -555,9 +558,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
 #pragma unroll
             for (int h = 0; h < W / 8; ++h) {
-              const long long off = img_off(i0 + 8 * h);
+              const uint32_t off = img_off(i0 + 8 * h);
               uint4 hv, lv;
-              split_hilo8(ms + 8 * h, hv, lv, last);
+              if (last)  // uniform: only the final sweep writes the +-1 configuration
+                split_hilo8(ms + 8 * h, hv, lv, true);
+              else
+                split_hilo8(ms + 8 * h, hv, lv, false);
 #if defined(NMFA_DBG_NOLO)
               st_hint(a_next + off, hv, pol_keep);
               if (lv.x == 0x12345u && lv.y == 7u) a.lo[0] = 1;
@@ -772,6 +778,11 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->k_last_sub = (n - (ds->kblocks - 1) * kBK + 15) / 16;
   ds->Rp = (pl->R + 255) / 256 * 256;
   const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  if (img_bytes >= (1ULL << 32)) {  // the epilogue addresses images with 32-bit offsets
+    set_error("dense plan: n x replicas too large for one plan (state image >= 4 GiB); "
+              "split the replicas over several calls (r0)");
+    return NMFA_ERR_ARG;
+  }
   NMFA_CUDA_TRY(cudaMalloc(&ds->lo_img, img_bytes));
   NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[0], img_bytes));
   NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[1], img_bytes));
