@@ -263,7 +263,7 @@ def run_sk65536(args):
     R = args.reads or R
     params = NmfaParams(t_f=t_f, seed=args.seed)
     t0 = time.perf_counter()
-    sk = RowShardedSK(n, 7, R, params, device=local)
+    sk = RowShardedSK(n, 7, R, params, device=local, exchange=args.exchange)
     torch.cuda.synchronize(dev)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream(dev)
@@ -317,6 +317,9 @@ def run_sk65536(args):
             "data": "synthetic (on-device Philox SK couplings)",
             "config": {"workload": desc, "reads_total": R, "n": n, "t_f": t_f,
                        "parallelism": f"J row-sharded x{world}", "setup_s": setup_s,
+                       "exchange": (f"{args.exchange}: " + ("epilogue peer stores into symmetric "
+                                    "memory + device barrier per sweep" if args.exchange == "p2p"
+                                    else "NCCL all_gather_into_tensor per sweep")),
                        "l2": "J shard (8.6/G GB) exceeds L2; no flush needed",
                        "best_energy": best, "best_energy_per_spin": best / n},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
@@ -584,6 +587,8 @@ def main():
     ap.add_argument("--ref-runs", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the SK100 TTS99 side measurement")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="sk65536: fused peer-store exchange (default) or NCCL all-gather")
     args = ap.parse_args()
     if args.workload == "ground26":
         run_ground(args, args.impl)

@@ -125,6 +125,18 @@ int nmfa_plan_image_info(const nmfa_plan_t* plan, void** image0, void** image1,
                          int64_t* slice_bytes, int32_t* n_slices, int32_t* slice_lo,
                          int32_t* slice_hi);
 
+/* Fused exchange for a row-sharded plan (replaces the per-sweep all-gather):
+ * image0_ptrs / image1_ptrs hold, for every shard g < world, a device pointer
+ * to shard g's operand image of each sweep parity (peer-accessible memory, e.g.
+ * CUDA IPC / symmetric-memory buffers of >= bytes each; the plan adopts
+ * entries [rank] as its own images and does not free them).  Each sweep's
+ * epilogue then stores every new hi line into all shards' images directly, so
+ * the exchange overlaps the GEMM.  Between nmfa_plan_run_sweeps calls the
+ * caller must synchronise the shards (a device-side barrier after each
+ * sweep).  world <= 8. */
+int nmfa_plan_set_exchange(nmfa_plan_t* plan, void* const* image0_ptrs, void* const* image1_ptrs,
+                           int32_t world, int32_t rank, int64_t bytes);
+
 /* +-1 configurations [n_reads][n] from the (all-gathered) sign image that the
  * last sweep t_f-1 wrote (parity t_f & 1). */
 int nmfa_plan_read_config(const nmfa_plan_t* plan, int8_t* config_dev, void* stream);

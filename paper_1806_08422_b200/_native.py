@@ -44,6 +44,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "nmfa_plan_read_config": (_i32, [_p, _p, _p]),
     "nmfa_anneal_many": (_i32, [_p, _i32, _i64, _i32, _p, _f64, _f64, _p, _p, _p, _p]),
+    "nmfa_plan_set_exchange": (_i32, [_p, _p, _p, _i32, _i32, _i64]),
     "nmfa_gset_parse": (_i32, [ctypes.c_char_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                _p, _p, _p, _i64]),
     "nmfa_ground_state": (_i32, [_p, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_i64), _p]),

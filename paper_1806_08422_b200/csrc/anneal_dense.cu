@@ -70,6 +70,8 @@ struct DenseTile {
   int m_blk, n0, nlen, pad;
 };
 
+constexpr int kMaxPeers = 7;  // other shards of a fused-exchange plan (8 GPUs)
+
 struct DenseState {
   int np = 0, kp = 0, kblocks = 0, k_last_sub = 0, pairs = 0;
   int slice_lo = 0, slice_hi = 0;  // k-slices of the image this device writes
@@ -86,6 +88,12 @@ struct DenseState {
   CUtensorMap tmA[2];
   CUtensorMap tmB[2];  // B boxes of exactly one tile half (2 x rows lines), the two widths
   int bhalf[2] = {0, 0};
+  // fused exchange (row-sharded J): the operand images are peer-accessible
+  // buffers owned by the caller, and the epilogue also stores every new hi
+  // line into the other shards' images at the same offset
+  bool external_images = false;
+  int n_peers = 0;
+  uint8_t* peer_img[2][kMaxPeers] = {};
 };
 
 struct DenseStepArgs {
@@ -117,6 +125,9 @@ struct DenseStepArgs {
   unsigned long long* tl2;    // debug: globaltimer per (pair, tile) (NMFA_TRACE2)
   const int16_t* korder;      // [tile][kblocks] K order, or null for natural order
   int bhalf0, bhalf1;         // rows per CTA of the two tile widths (B box sizes)
+  int n_peers;                // fused exchange: other shards' images (same layout)
+  uint8_t* peer0[kMaxPeers];
+  uint8_t* peer1[kMaxPeers];
   unsigned long long* tl3;    // debug: per k-slice clock64 of CTA 0 (NMFA_TRACE3)
 };
 
@@ -570,6 +581,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
 #elif !defined(NMFA_DBG_NOMEM)
               st_hint(a_next + off, hv, pol_keep);
               st_hint(a.lo + off, lv, pol_stream);
+              // fused exchange: the same 16 bytes into every other shard's image
+              // (NVLink peer stores, overlapped with the GEMM of the next tile)
+              for (int pk = 0; pk < a.n_peers; ++pk)
+                *reinterpret_cast<uint4*>(((t & 1) ? a.peer0[pk] : a.peer1[pk]) + off) = hv;
 #else
               if (hv.x == 0x12345u && lv.y == 7u) a.lo[0] = 1;
 #endif
@@ -756,8 +771,10 @@ void dense_plan_free(nmfa_plan* pl) {
   auto* ds = static_cast<DenseState*>(pl->dense);
   if (!ds) return;
   if (ds->lo_img) cudaFree(ds->lo_img);
-  if (ds->a_img[0]) cudaFree(ds->a_img[0]);
-  if (ds->a_img[1]) cudaFree(ds->a_img[1]);
+  if (!ds->external_images) {
+    if (ds->a_img[0]) cudaFree(ds->a_img[0]);
+    if (ds->a_img[1]) cudaFree(ds->a_img[1]);
+  }
   if (ds->d_tiles) cudaFree(ds->d_tiles);
   if (ds->d_tile_off) cudaFree(ds->d_tile_off);
   if (ds->d_kneed) cudaFree(ds->d_kneed);
@@ -1054,6 +1071,11 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   auto kern = noise ? dense_anneal_kernel<true> : dense_anneal_kernel<false>;
   a.bhalf0 = ds->bhalf[0];
   a.bhalf1 = ds->bhalf[1];
+  a.n_peers = ds->n_peers;
+  for (int k = 0; k < kMaxPeers; ++k) {
+    a.peer0[k] = ds->peer_img[0][k];
+    a.peer1[k] = ds->peer_img[1][k];
+  }
   NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1], a));
   add_launches(launches);
   if (tl3_path) {
@@ -1096,6 +1118,56 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
       }
       fclose(f);
     }
+  }
+  return NMFA_OK;
+}
+
+// Fused exchange for a row-sharded plan: adopt the caller's peer-accessible
+// buffers as this shard's operand images (images[p][rank]) and record the
+// other shards' images as store targets.  The caller synchronises the shards
+// between sweeps (every shard's stores must land before the next sweep reads).
+int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int world, int rank,
+                       int64_t bytes) {
+  auto* ds = static_cast<DenseState*>(pl->dense);
+  if (!ds) {
+    set_error("not a dense plan");
+    return NMFA_ERR_STATE;
+  }
+  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  if (world < 1 || world > kMaxPeers + 1 || rank < 0 || rank >= world) {
+    set_error("fused exchange needs 1 <= world <= 8 and 0 <= rank < world");
+    return NMFA_ERR_ARG;
+  }
+  if (bytes < (int64_t)img_bytes) {
+    set_error("exchange buffers smaller than the plan's operand image (" +
+              std::to_string(img_bytes) + " bytes)");
+    return NMFA_ERR_ARG;
+  }
+  for (int g = 0; g < world; ++g)
+    if (!img0[g] || !img1[g]) {
+      set_error("NULL exchange buffer");
+      return NMFA_ERR_ARG;
+    }
+  const bool own = img0[rank] == ds->a_img[0] && img1[rank] == ds->a_img[1];
+  if (!own) {  // adopt the caller's buffers (not freed by the plan)
+    if (!ds->external_images) {
+      cudaFree(ds->a_img[0]);
+      cudaFree(ds->a_img[1]);
+    }
+    ds->external_images = true;
+    ds->a_img[0] = static_cast<uint8_t*>(img0[rank]);
+    ds->a_img[1] = static_cast<uint8_t*>(img1[rank]);
+  }
+  int err;
+  for (int b = 0; b < 2; ++b)
+    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
+      return err;
+  ds->n_peers = 0;
+  for (int g = 0; g < world; ++g) {
+    if (g == rank) continue;
+    ds->peer_img[0][ds->n_peers] = static_cast<uint8_t*>(img0[g]);
+    ds->peer_img[1][ds->n_peers] = static_cast<uint8_t*>(img1[g]);
+    ++ds->n_peers;
   }
   return NMFA_OK;
 }

@@ -563,6 +563,18 @@ int nmfa_plan_image_info(const nmfa_plan_t* pl, void** img0, void** img1, int64_
   return dense_image_info(pl, img0, img1, slice_bytes, n_slices, slice_lo, slice_hi);
 }
 
+int nmfa_plan_set_exchange(nmfa_plan_t* pl, void* const* image0_ptrs, void* const* image1_ptrs,
+                           int32_t world, int32_t rank, int64_t bytes) {
+  if (!pl || !image0_ptrs || !image1_ptrs) return arg_error("NULL argument");
+  if (pl->p->path != NMFA_PATH_DENSE) return arg_error("the fused exchange is a dense-path feature");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->p->device);
+  const int err = dense_set_exchange(pl, image0_ptrs, image1_ptrs, world, rank, bytes);
+  cudaSetDevice(prev);
+  return err;
+}
+
 int nmfa_plan_read_config(const nmfa_plan_t* pl, int8_t* cfg, void* stream) {
   if (!pl || !cfg) return arg_error("NULL argument");
   int prev = 0;

@@ -122,6 +122,8 @@ int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R
                              const uint64_t* key_bases, int8_t* cfg, cudaStream_t st);
 int gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out, int64_t* ei,
                int64_t* ej, double* w, int64_t cap);
+int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int world, int rank,
+                       int64_t bytes);
 int ground_state(const nmfa_problem* p, int max_n, double* energy, int64_t* degeneracy,
                  int8_t* config);
 bool dense_is_sharded(const nmfa_problem* p);

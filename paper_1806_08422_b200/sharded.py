@@ -10,9 +10,15 @@ rank, NCCL over NVLink).  Energies are per-shard partials of
 The reference has no counterpart (its dense J is an n x n float64 matrix,
 problem.py:100-104, infeasible at N = 65,536); this is the §8(e) scaling mode.
 On one GPU the problem is unsharded and the whole anneal is one persistent
-launch; with G > 1 a sweep is one launch followed by one in-place
-all-gather.  Noise is keyed by the global replica and spin index and the K
-order is fixed, so results do not depend on G.
+launch.  With G > 1 a sweep is one launch followed by the exchange:
+  exchange="nccl"  one in-place NCCL all-gather of the sweep's image;
+  exchange="p2p"   fused: the operand images live in symmetric (peer-mapped)
+                   memory and each sweep's epilogue stores every new state
+                   line into all G images itself (nmfa_plan_set_exchange), so
+                   the transfer overlaps the GEMM; a device-side barrier
+                   separates sweeps.
+Noise is keyed by the global replica and spin index and the K order is fixed,
+so results do not depend on G or on the exchange.
 """
 
 from __future__ import annotations
@@ -34,6 +40,29 @@ def row_shard(n, world, rank, align=128):
                          f"got n = {n}")
     per = n // world
     return rank * per, (rank + 1) * per
+
+
+def _default_group():
+    import torch.distributed as dist
+    return dist.group.WORLD
+
+
+def link_images(shard, ptrs, world, rank, nbytes):
+    """Point `shard`'s plan at every shard's operand images: ptrs[p][g] is shard
+    g's image of sweep parity p.  Entry [rank] becomes the shard's own image."""
+    P = ctypes.c_void_p * world
+    _native.check(_native.load().nmfa_plan_set_exchange(
+        shard.plan, ctypes.cast(P(*ptrs[0]), ctypes.c_void_p),
+        ctypes.cast(P(*ptrs[1]), ctypes.c_void_p), int(world), int(rank), int(nbytes)))
+
+
+def link_local_shards(shards):
+    """Single-process emulation of the fused exchange: shards that live on one
+    device store straight into each other's images (tests; one GPU)."""
+    G = len(shards)
+    ptrs = [[s.images[p].data_ptr() for s in shards] for p in range(2)]
+    for g, s in enumerate(shards):
+        link_images(s, ptrs, G, g, s.images[0].numel())
 
 
 class _CudaBytes:
@@ -80,7 +109,8 @@ class ShardedResult:
 class RowShardedSK:
     """Synthetic SK instance with J row-sharded over the ranks of `group`."""
 
-    def __init__(self, n, seed, n_reads, params=None, group=None, device=None, shard=None):
+    def __init__(self, n, seed, n_reads, params=None, group=None, device=None, shard=None,
+                 exchange="nccl"):
         import torch
         import torch.distributed as dist
 
@@ -118,6 +148,27 @@ class RowShardedSK:
         dev = torch.device("cuda", self.device)
         nbytes = self.slice_bytes * self.n_slices
         self.images = [torch.as_tensor(_CudaBytes(p.value, nbytes), device=dev) for p in (i0, i1)]
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
+        self.exchange = exchange
+        self._symm = None
+        if exchange == "p2p" and self.world > 1 and shard is None:
+            self._setup_p2p(nbytes, dev)
+
+    def _setup_p2p(self, nbytes, dev):
+        """Symmetric-memory images + pointer exchange (nmfa_plan_set_exchange)."""
+        import torch
+        from torch.distributed import _symmetric_memory as symm_mem
+
+        bufs = [symm_mem.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        hdls = [symm_mem.rendezvous(b, self.group or _default_group()) for b in bufs]
+        link_images(self, [h.buffer_ptrs for h in hdls], self.world, self.rank, nbytes)
+        self.images = bufs
+        self._symm = (bufs, hdls)
+
+    def _barrier(self):
+        """Every shard's stores of this sweep are visible before the next one reads."""
+        self._symm[1][0].barrier(channel=0)
 
     # -- the protocol, one piece at a time (run() strings them together) --
     def _stream(self, stream):
@@ -157,8 +208,11 @@ class RowShardedSK:
             for t in range(t_f):
                 self.sweeps(seed, t, t + 1, r0, stream=stream)
                 with torch.cuda.stream(stream):
-                    exchange_slices(self.images[(t + 1) & 1], self.slice_lo, self.slice_hi,
-                                    self.slice_bytes, self.group)
+                    if self._symm is not None:
+                        self._barrier()
+                    else:
+                        exchange_slices(self.images[(t + 1) & 1], self.slice_lo, self.slice_hi,
+                                        self.slice_bytes, self.group)
             self.sweeps(seed, t_f, t_f, r0, energy=en, stream=stream)
             with torch.cuda.stream(stream):
                 allreduce_sum(en, self.group)

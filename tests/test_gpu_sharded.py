@@ -93,3 +93,38 @@ def test_sharded_problem_guards():
     assert lib.nmfa_problem_set_path(s.problem, _native.PATH_SPARSE) != 0
     with pytest.raises(ValueError):
         RowShardedSK(1000, 1, 256, nb.NmfaParams(t_f=10), shard=(2, 0))
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_fused_exchange_equals_unsharded(G):
+    """Fused exchange (nmfa_plan_set_exchange): each shard's epilogue stores its
+    new state lines into every shard's image, no separate all-gather.  Shards
+    run one after another on one device; results must equal G = 1 bit for bit."""
+    from paper_1806_08422_b200.sharded import link_local_shards
+    n, sk_seed, R, params = 512, 4, 256, nb.NmfaParams(t_f=60, seed=21)
+    ref = RowShardedSK(n, sk_seed, R, params).run(params.seed)
+    shards = [RowShardedSK(n, sk_seed, R, params, shard=(G, g)) for g in range(G)]
+    link_local_shards(shards)
+    for t in range(params.t_f):
+        for s in shards:
+            s.sweeps(params.seed, t, t + 1)
+    parts = []
+    for s in shards:
+        e = torch.empty(R, dtype=torch.float64, device="cuda")
+        s.sweeps(params.seed, params.t_f, params.t_f, energy=e)
+        parts.append(e)
+    for s in shards:
+        assert torch.equal(s.read_config(), ref.configs)
+    assert torch.equal(torch.stack(parts).sum(0), ref.energies)
+
+
+def test_fused_exchange_argument_checks():
+    lib = _native.load()
+    s = RowShardedSK(512, 1, 256, nb.NmfaParams(t_f=10, seed=0), shard=(2, 0))
+    P = ctypes.c_void_p * 2
+    ptr = ctypes.c_void_p(s.images[0].data_ptr())
+    good = P(ptr, ptr)
+    assert lib.nmfa_plan_set_exchange(s.plan, ctypes.cast(good, ctypes.c_void_p),
+                                      ctypes.cast(good, ctypes.c_void_p), 9, 0, 1 << 30) != 0
+    assert lib.nmfa_plan_set_exchange(s.plan, ctypes.cast(good, ctypes.c_void_p),
+                                      ctypes.cast(good, ctypes.c_void_p), 2, 0, 16) != 0
