@@ -503,6 +503,10 @@ def run_ours(args):
                 "kernel": f"{info['path']} NMFA step (tcgen05, fused epilogue)",
                 "algorithmic_per_launch": f"2*N^2*R = {flop:.4g} FLOP (N={n}, R={R}; padded N={npad})",
                 "avg_launch_us": per_launch_s * 1e6, "peak_source": f"{peak_src} bf16 sustained"}
+        if info["path"] == "small":
+            roof["note"] = ("n <= 256 runs on chip for all t_f steps; the binding resource is the fused "
+                            "update's instruction issue (ncu: 28 instructions per spin-update, IPC 2.1 "
+                            "of 4), not the tensor pipe (profiles/r01/ncu_full_summary.json)")
     else:
         nnz = 2 * p.num_edges
         byts = R * n * 8 + nnz * 8 + (n + 1) * 4
