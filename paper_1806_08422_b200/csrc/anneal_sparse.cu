@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(cons
   // Memory-level parallelism: the group's 9 row pointers come from one
   // cooperative load; then every gather of the 8 spins is issued before the
   // first use (degree <= kFast unrolled, longer rows in a general loop).
-  constexpr int kFast = 3;  // cubic / Moebius / ladder degree; longer rows loop
+  constexpr int kFast = 3;  // unrolled row length (cubic / Moebius ladder); longer rows loop
   const int i_base = 8 * q;
   const int pl = lane <= 8 ? __ldg(a.ptr + min(i_base + lane, n)) : 0;
   int k0[8], deg[8];
@@ -65,21 +65,49 @@ __global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(cons
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) sold[qq] = (i_base + qq < n) ? so[(i_base + qq) * Rp] : 0.f;
   float v[8][kFast];
-#pragma unroll
-  for (int qq = 0; qq < 8; ++qq)
-#pragma unroll
-    for (int u = 0; u < kFast; ++u)
-      v[qq][u] = u < deg[qq] ? so[__ldg(idx + k0[qq] + u) * Rp] : 0.f;
   float acc[8];
+  const int K0 = k0[0], seg = k0[7] + deg[7] - K0;  // the group's CSR entries [K0, K0 + seg)
+  bool fast = seg <= 32;
 #pragma unroll
-  for (int qq = 0; qq < 8; ++qq) {
-    float s2 = 0.f;
+  for (int qq = 0; qq < 8; ++qq) fast = fast && deg[qq] <= kFast;
+  if (fast) {
+    // lanes hold the segment's element offsets (idx * Rp) and weights; every
+    // gather broadcasts its entry by shuffle (no per-lane index arithmetic)
+    const int off_l = lane < seg ? __ldg(idx + K0 + lane) * Rp : 0;
+    const float w_l = lane < seg ? __ldg(wts + K0 + lane) : 0.f;
 #pragma unroll
-    for (int u = 0; u < kFast; ++u)
-      if (u < deg[qq]) s2 = fmaf(__ldg(wts + k0[qq] + u), v[qq][u], s2);  // uniform: L1 broadcast
-    for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k)  // rows longer than kFast
-      s2 = fmaf(__ldg(wts + k), so[__ldg(idx + k) * Rp], s2);
-    acc[qq] = s2;
+    for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+      for (int u = 0; u < kFast; ++u) {
+        const int off = __shfl_sync(0xffffffffu, off_l, (k0[qq] - K0 + u) & 31);
+        v[qq][u] = u < deg[qq] ? so[off] : 0.f;
+      }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      float s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < kFast; ++u) {
+        const float wv = __shfl_sync(0xffffffffu, w_l, (k0[qq] - K0 + u) & 31);
+        if (u < deg[qq]) s2 = fmaf(wv, v[qq][u], s2);  // CSR order, like the general path
+      }
+      acc[qq] = s2;
+    }
+  } else {
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+      for (int u = 0; u < kFast; ++u)
+        v[qq][u] = u < deg[qq] ? so[__ldg(idx + k0[qq] + u) * Rp] : 0.f;
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      float s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < kFast; ++u)
+        if (u < deg[qq]) s2 = fmaf(__ldg(wts + k0[qq] + u), v[qq][u], s2);  // uniform: L1 broadcast
+      for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k)  // rows longer than kFast
+        s2 = fmaf(__ldg(wts + k), so[__ldg(idx + k) * Rp], s2);
+      acc[qq] = s2;
+    }
   }
   const bool valid = r < a.R;
   float z[8];
