@@ -1,6 +1,8 @@
 // C-ABI layer: problem construction (problem.py:25-116 restated in C++),
 // plans, dispatch to the kernel paths, errors.  See include/nmfa_b200.h.
 #include <algorithm>
+#include <new>
+#include <stdexcept>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -53,11 +55,30 @@ using namespace nmfa;
 
 extern "C" {
 
+// Every entry point converts C++ exceptions (host allocation failures above
+// all) into status codes: nothing may unwind across the C ABI.
+#define NMFA_API_BEGIN try {
+#define NMFA_API_END                                                          \
+  }                                                                           \
+  catch (const std::bad_alloc&) {                                             \
+    nmfa::set_error("host out of memory");                                    \
+    return NMFA_ERR_STATE;                                                    \
+  }                                                                           \
+  catch (const std::exception& ex) {                                          \
+    nmfa::set_error(std::string("internal error: ") + ex.what());             \
+    return NMFA_ERR_STATE;                                                    \
+  }                                                                           \
+  catch (...) {                                                               \
+    nmfa::set_error("internal error");                                        \
+    return NMFA_ERR_STATE;                                                    \
+  }
+
 const char* nmfa_last_error(void) { return g_err.c_str(); }
 const char* nmfa_version(void) { return "nmfa_b200 0.1.0 (sm_100a)"; }
 int64_t nmfa_last_launch_count(void) { return g_launches; }
 
 int nmfa_problem_destroy(nmfa_problem_t* p) {
+  NMFA_API_BEGIN
   if (!p) return NMFA_OK;
   if (p->cached_plan) nmfa_plan_destroy(p->cached_plan);
   if (p->host_cfg) cudaFree(p->host_cfg);
@@ -73,11 +94,13 @@ int nmfa_problem_destroy(nmfa_problem_t* p) {
   cudaSetDevice(prev);
   delete p;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const int64_t* ej_in,
                         const double* w_in, const double* h_in, int32_t device,
                         nmfa_problem_t** out) {
+  NMFA_API_BEGIN
   if (!out) return arg_error("out pointer is NULL");
   *out = nullptr;
   // ---- validation, problem.py:25-62 ----
@@ -272,10 +295,12 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
   }
   *out = p;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int64_t row_hi,
                                   int32_t device, nmfa_problem_t** out) {
+  NMFA_API_BEGIN
   if (!out) return arg_error("out pointer is NULL");
   *out = nullptr;
   if (n < 2) return arg_error("sk generator needs n >= 2, got " + std::to_string(n));
@@ -325,9 +350,11 @@ int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int6
   }
   *out = p;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
+  NMFA_API_BEGIN
   if (!p || !info) return arg_error("NULL argument");
   info->n = p->n;
   info->n_edges = p->n_edges;
@@ -338,9 +365,11 @@ int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
   info->int_weights = p->int_weights;
   info->j_scale = p->j_scale;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
+  NMFA_API_BEGIN
   if (!p) return arg_error("NULL problem");
   if (p->device_generated && path != NMFA_PATH_DENSE)
     return arg_error("a device-generated problem only runs the dense path");
@@ -377,9 +406,11 @@ int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
   if (path < 0 || path > 2) return arg_error("unknown path");
   p->path = path;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_plan_destroy(nmfa_plan_t* pl) {
+  NMFA_API_BEGIN
   if (!pl) return NMFA_OK;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -392,10 +423,12 @@ int nmfa_plan_destroy(nmfa_plan_t* pl) {
   cudaSetDevice(prev);
   delete pl;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_plan_create(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
                      double alpha, double sigma, nmfa_plan_t** out) {
+  NMFA_API_BEGIN
   if (!p || !out) return arg_error("NULL argument");
   *out = nullptr;
   if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
@@ -452,11 +485,13 @@ int nmfa_plan_create(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
   }
   *out = pl;
   return NMFA_OK;
+  NMFA_API_END
 }
 
 int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise,
                   const float* s0, int8_t* cfg, double* energy, float* s_out, float* s_hist,
                   double* e_hist, void* stream) {
+  NMFA_API_BEGIN
   if (!pl) return arg_error("NULL plan");
   if (!cfg) return arg_error("config output is NULL");
   if (e_hist && !s_hist) return arg_error("e_hist requires s_hist");
@@ -508,11 +543,13 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
   }
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_plan_run_sweeps(nmfa_plan_t* pl, uint64_t seed, int64_t r0, int32_t t_begin,
                          int32_t t_end, int32_t energy_pass, int8_t* cfg, double* energy,
                          void* stream) {
+  NMFA_API_BEGIN
   if (!pl) return arg_error("NULL plan");
   const nmfa_problem* p = pl->p;
   if (p->path != NMFA_PATH_DENSE) return arg_error("sweep ranges are a dense-path feature");
@@ -534,18 +571,22 @@ int nmfa_plan_run_sweeps(nmfa_plan_t* pl, uint64_t seed, int64_t r0, int32_t t_b
                                    (cudaStream_t)stream);
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out,
                     int64_t* edges_i, int64_t* edges_j, double* weights, int64_t cap) {
+  NMFA_API_BEGIN
   if (!text || len < 0 || !n_out || !m_out) return arg_error("NULL argument");
   if ((edges_i || edges_j || weights) && !(edges_i && edges_j && weights))
     return arg_error("edge arrays must be all NULL (header query) or all set");
   return gset_parse(text, len, n_out, m_out, edges_i, edges_j, weights, cap);
+  NMFA_API_END
 }
 
 int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy,
                       int64_t* degeneracy, int8_t* config) {
+  NMFA_API_BEGIN
   if (!p || !energy || !degeneracy) return arg_error("NULL argument");
   int prev = 0;
   cudaGetDevice(&prev);
@@ -554,17 +595,21 @@ int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy,
   const int err = ground_state(p, max_n, energy, degeneracy, config);
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_plan_image_info(const nmfa_plan_t* pl, void** img0, void** img1, int64_t* slice_bytes,
                          int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi) {
+  NMFA_API_BEGIN
   if (!pl || !img0 || !img1 || !slice_bytes || !n_slices || !slice_lo || !slice_hi)
     return arg_error("NULL argument");
   return dense_image_info(pl, img0, img1, slice_bytes, n_slices, slice_lo, slice_hi);
+  NMFA_API_END
 }
 
 int nmfa_plan_set_exchange(nmfa_plan_t* pl, void* const* image0_ptrs, void* const* image1_ptrs,
                            int32_t world, int32_t rank, int64_t bytes) {
+  NMFA_API_BEGIN
   if (!pl || !image0_ptrs || !image1_ptrs) return arg_error("NULL argument");
   if (pl->p->path != NMFA_PATH_DENSE) return arg_error("the fused exchange is a dense-path feature");
   int prev = 0;
@@ -573,9 +618,11 @@ int nmfa_plan_set_exchange(nmfa_plan_t* pl, void* const* image0_ptrs, void* cons
   const int err = dense_set_exchange(pl, image0_ptrs, image1_ptrs, world, rank, bytes);
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_plan_read_config(const nmfa_plan_t* pl, int8_t* cfg, void* stream) {
+  NMFA_API_BEGIN
   if (!pl || !cfg) return arg_error("NULL argument");
   int prev = 0;
   cudaGetDevice(&prev);
@@ -583,12 +630,14 @@ int nmfa_plan_read_config(const nmfa_plan_t* pl, int8_t* cfg, void* stream) {
   const int err = dense_read_config(pl, cfg, (cudaStream_t)stream);
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_anneal(const nmfa_problem_t* cp, int64_t R, int32_t t_f, const double* temps,
                 double alpha, double sigma, uint64_t seed, int64_t r0, const float* noise,
                 const float* s0, int8_t* cfg, double* energy, float* s_out, float* s_hist,
                 double* e_hist, void* stream) {
+  NMFA_API_BEGIN
   if (!cp) return arg_error("NULL problem");
   if (!temps || t_f < 1) return arg_error("t_f must be at least 1, got " + std::to_string(t_f));
   auto* p = const_cast<nmfa_problem*>(cp);  // only the plan cache is mutated
@@ -619,11 +668,13 @@ int nmfa_anneal(const nmfa_problem_t* cp, int64_t R, int32_t t_f, const double* 
     err = NMFA_ERR_CUDA;
   }
   return err;
+  NMFA_API_END
 }
 
 int nmfa_anneal_many(const nmfa_problem_t* const* ps, int32_t count, int64_t R, int32_t t_f,
                      const double* temps, double alpha, double sigma, const uint64_t* seeds,
                      int8_t* cfg, double* energy, void* stream) {
+  NMFA_API_BEGIN
   if (!ps || !seeds || !cfg || count < 1) return arg_error("NULL argument or empty instance list");
   if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
   if (!temps || t_f < 1) return arg_error("t_f must be at least 1, got " + std::to_string(t_f));
@@ -695,11 +746,13 @@ int nmfa_anneal_many(const nmfa_problem_t* const* ps, int32_t count, int64_t R, 
   }
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const double* temps,
                      double alpha, double sigma, uint64_t seed, int64_t r0, int8_t* cfg_host,
                      double* energy_host) {
+  NMFA_API_BEGIN
   if (!p || !cfg_host) return arg_error("NULL argument");
   if (R < 1) return arg_error("n_runs must be at least 1, got " + std::to_string(R));
   static const bool timing = getenv("NMFA_TIMING") != nullptr;
@@ -753,10 +806,12 @@ int nmfa_anneal_host(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
             ms(t1, t2), ms(t2, t3));
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_energy(const nmfa_problem_t* p, const int8_t* cfg, int64_t n_cfg, double* energy,
                 void* stream) {
+  NMFA_API_BEGIN
   if (!p || !cfg || !energy) return arg_error("NULL argument");
   if (p->device_generated)
     return arg_error("a device-generated problem has no edge list; its energies come from "
@@ -781,12 +836,15 @@ int nmfa_energy(const nmfa_problem_t* p, const int8_t* cfg, int64_t n_cfg, doubl
   if (part) cudaFreeAsync(part, st);
   cudaSetDevice(prev);
   return err;
+  NMFA_API_END
 }
 
 int nmfa_best_of(const double* e, int64_t n, double* best_e, int64_t* best_i, void* stream) {
+  NMFA_API_BEGIN
   if (!e || !best_e || !best_i) return arg_error("NULL argument");
   if (n < 1) return arg_error("best-of needs at least one energy");
   return launch_best_of(e, n, best_e, best_i, (cudaStream_t)stream);
+  NMFA_API_END
 }
 
 }  // extern "C"
