@@ -57,3 +57,21 @@ def test_problem_create_rejects_bad_arguments(lib):
                                               _native.ptr(w), None, 0, ctypes.byref(out)))
     with pytest.raises(ValueError, match="positive"):
         _native.check(lib.nmfa_problem_create(0, 0, None, None, None, None, 0, ctypes.byref(out)))
+
+
+def test_backend_matches_reference_operator_signatures():
+    """paper_1806_08422_b200.kernels has the reference backend's call signatures
+    (kernels.py:30-32) -- checked against the installed reference when present."""
+    import inspect
+    import os
+    import sys
+
+    from paper_1806_08422_b200 import kernels as b200
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "nmfa")):
+        pytest.skip("reference package not installed in baseline/_ref")
+    sys.path.insert(0, ref)
+    from nmfa import _kernels_numpy as refk
+    for name in ("anneal_dense", "anneal_sparse", "gray_ground"):
+        assert list(inspect.signature(getattr(b200, name)).parameters) == \
+            list(inspect.signature(getattr(refk, name)).parameters), name
