@@ -16,15 +16,34 @@
 // spins, a warp covers four full 128-B lines), so no transpose pass exists.
 //
 // Roles per CTA (640 threads): warps 0-15 epilogue (lane quarter x column
-// quarter; 4 warps per scheduler to hide the Philox/MUFU latency chains),
+// part; 4 warps per scheduler to hide the Philox/MUFU latency chains),
 // warp 16 TMA producer, warp 17 MMA issuer (leader CTA only), warp 18 TMEM
 // allocator.  The control roles take the HIGHEST warp ids on purpose: the
 // warp scheduler favours high ids, and with low ids the producer and MMA
 // issuer starved behind the epilogue warps (measured: 3x longer k-block
-// intervals, see profiles/).  6-stage smem ring (A 16 KB + B <=16 KB per stage), 2 TMEM
-// accumulator slots of 256 columns so the epilogue of tile j overlaps the MMAs
-// of tile j+1.  Each pair owns a contiguous slice of the (replica block,
-// 16-spin unit) space, balanced to within one unit across the 74 pairs.
+// intervals, see profiles/).  3-stage smem ring (A: one 32 KB box; B: one box
+// of exactly the tile half, <= 32 KB), 2 TMEM accumulator slots of 256
+// columns so the epilogue of tile j overlaps the MMAs of tile j+1.
+//
+// Persistence: one cooperative launch runs every sweep of the anneal (plus the
+// exact energy pass).  Each pair owns a contiguous run of (replica block, spin
+// range) tiles in m-major order, balanced to whole tiles by a cost model of
+// the MMA and TMA time per k-slice.  Instead of a kernel boundary between
+// sweeps, every warp publishes the k-slices it wrote in per-(replica block,
+// k-slice) readiness counters, and producers wait only for the slices they
+// are about to load; the K order is natural so results do not depend on the
+// schedule, the replica count or the row sharding.
+//
+// Experiment switches (measurements in profiles/r01/, none changes results
+// unless noted):
+//   env NMFA_TILE_ORDER = mmajor | sorted | spin | block | alt | rev  (tile dealing)
+//   env NMFA_KORDER = early    (earliest-published-slice-first K order; results
+//                               then depend on the schedule)
+//   env NMFA_TILE_W = 1..16    (force the tile width in 16-spin units)
+//   env NMFA_TRACE / NMFA_TRACE2 / NMFA_TRACE3 = <file>  (clock64/globaltimer traces)
+//   -DNMFA_DBG_NOEPI / NOMEM / NOLOAD / NOLO / NOMATH / NOTMEM / NOMUFU / SPREAD /
+//    PLAINMEM / LOKEEP  (epilogue ablations for timing; results are wrong)
+//   -DNMFA_EPI_PREFETCH, -DNMFA_EPI_WARPS=n, -DNMFA_DSTAGES=n, -DNMFA_ROLES_FIRST
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
