@@ -7,6 +7,8 @@
 // matches the Philox counter granularity, so one Philox call per thread
 // feeds its eight spins (common.cuh noise identity).
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -35,19 +37,35 @@ struct SparseStepArgs {
   int last;
 };
 
-__global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(const SparseStepArgs a) {
+// V replicas per lane (1 or 2): with V = 2 every state access is one float2,
+// halving the per-update address arithmetic and the uniform CSR overhead of
+// the V = 1 layout (the CSR path is issue-bound; profiles/r01/korder_ab.log).
+// Per replica the arithmetic and summation order are the same for any V.
+template <int V>
+__global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
+    sparse_step_kernel(const SparseStepArgs a) {
+  using Vec = typename std::conditional<V == 2, float2, float>::type;
   // grid (replica-group blocks, spin groups): warp w of block x owns replicas
-  // [32 (8x + w), +32) of spin group y, so consecutive blocks read the same
+  // [32V (8x + w), +32V) of spin group y, so consecutive blocks read the same
   // state rows (no index division; 32-bit element offsets, n * Rp < 2^31)
   const int lane = threadIdx.x & 31;
   const int rb = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int Rp = (int)a.Rp, n = a.n;
-  if (rb * 32 >= Rp) return;
+  if (rb * 32 * V >= Rp) return;
   const int q = blockIdx.y;
-  const int r = rb * 32 + lane;
+  const int r = (rb * 32 + lane) * V;  // this lane's first replica
   const float* __restrict__ so = a.s_old + r;
   const int* __restrict__ idx = a.idx;
   const float* __restrict__ wts = a.w;
+  auto ld = [&](int off, float* out) {  // V consecutive replicas of one state row
+    const Vec x = *reinterpret_cast<const Vec*>(so + off);
+    if constexpr (V == 2) {
+      out[0] = x.x;
+      out[1] = x.y;
+    } else {
+      out[0] = x;
+    }
+  };
 
   // Memory-level parallelism: the group's 9 row pointers come from one
   // cooperative load; then every gather of the 8 spins is issued before the
@@ -61,11 +79,18 @@ __global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(cons
     k0[qq] = __shfl_sync(0xffffffffu, pl, qq);
     deg[qq] = __shfl_sync(0xffffffffu, pl, qq + 1) - k0[qq];
   }
-  float sold[8];
+  float sold[8][V];
 #pragma unroll
-  for (int qq = 0; qq < 8; ++qq) sold[qq] = (i_base + qq < n) ? so[(i_base + qq) * Rp] : 0.f;
-  float v[8][kFast];
-  float acc[8];
+  for (int qq = 0; qq < 8; ++qq) {
+    if (i_base + qq < n) {
+      ld((i_base + qq) * Rp, sold[qq]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < V; ++c) sold[qq][c] = 0.f;
+    }
+  }
+  float v[8][kFast][V];
+  float acc[8][V];
   const int K0 = k0[0], seg = k0[7] + deg[7] - K0;  // the group's CSR entries [K0, K0 + seg)
   bool fast = seg <= 32;
 #pragma unroll
@@ -80,65 +105,109 @@ __global__ void __launch_bounds__(256, NMFA_SPARSE_MINB) sparse_step_kernel(cons
 #pragma unroll
       for (int u = 0; u < kFast; ++u) {
         const int off = __shfl_sync(0xffffffffu, off_l, (k0[qq] - K0 + u) & 31);
-        v[qq][u] = u < deg[qq] ? so[off] : 0.f;
+        if (u < deg[qq]) {
+          ld(off, v[qq][u]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
+        }
       }
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
-      float s2 = 0.f;
+      float s2[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) s2[c] = 0.f;
 #pragma unroll
       for (int u = 0; u < kFast; ++u) {
         const float wv = __shfl_sync(0xffffffffu, w_l, (k0[qq] - K0 + u) & 31);
-        if (u < deg[qq]) s2 = fmaf(wv, v[qq][u], s2);  // CSR order, like the general path
+        if (u < deg[qq])
+#pragma unroll
+          for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);  // CSR order
       }
-      acc[qq] = s2;
+#pragma unroll
+      for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
   } else {
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
-      for (int u = 0; u < kFast; ++u)
-        v[qq][u] = u < deg[qq] ? so[__ldg(idx + k0[qq] + u) * Rp] : 0.f;
+      for (int u = 0; u < kFast; ++u) {
+        if (u < deg[qq]) {
+          ld(__ldg(idx + k0[qq] + u) * Rp, v[qq][u]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
+        }
+      }
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
-      float s2 = 0.f;
+      float s2[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) s2[c] = 0.f;
 #pragma unroll
       for (int u = 0; u < kFast; ++u)
-        if (u < deg[qq]) s2 = fmaf(__ldg(wts + k0[qq] + u), v[qq][u], s2);  // uniform: L1 broadcast
-      for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k)  // rows longer than kFast
-        s2 = fmaf(__ldg(wts + k), so[__ldg(idx + k) * Rp], s2);
-      acc[qq] = s2;
-    }
-  }
-  const bool valid = r < a.R;
-  float z[8];
-  if (a.noise) {
+        if (u < deg[qq]) {
+          const float wv = __ldg(wts + k0[qq] + u);  // uniform: L1 broadcast
 #pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      const int i = i_base + qq;
-      z[qq] = (valid && i < n) ? a.noise[((long long)r * a.t_f + a.t) * n + i] : 0.f;
+          for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);
+        }
+      for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k) {  // rows longer than kFast
+        float x[V];
+        ld(__ldg(idx + k) * Rp, x);
+        const float wv = __ldg(wts + k);
+#pragma unroll
+        for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, x[c], s2[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
-  } else {
-    const unsigned long long key = a.key_base + (unsigned long long)r;
-    normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
-            bm_scale(a.sigma), z);
   }
-  float* __restrict__ sn = a.s_new + r;
   const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
-  const bool extra = valid && (a.s_hist != nullptr || a.last);
+  float* __restrict__ sn = a.s_new + r;
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const int rc = r + c;
+    const bool valid = rc < a.R;
+    float z[8];
+    if (a.noise) {
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const int i = i_base + qq;
+        z[qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
+      }
+    } else {
+      const unsigned long long key = a.key_base + (unsigned long long)rc;
+      normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
+              bm_scale(a.sigma), z);
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq)
+      acc[qq][c] = nmfa_update(acc[qq][c], __ldg(a.invn + min(i_base + qq, n - 1)),
+                               __ldg(a.hn + min(i_base + qq, n - 1)), z[qq], inv_t, alpha, oma,
+                               sold[qq][c]);
+    const bool extra = valid && (a.s_hist != nullptr || a.last);
+    if (extra) {
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const int i = i_base + qq;
+        if (i >= n) break;
+        const float sv = acc[qq][c];
+        if (a.s_hist) a.s_hist[((long long)rc * a.t_f + a.t) * n + i] = sv;
+        if (a.last) {
+          a.cfg[(long long)rc * n + i] = sv < 0.f ? (int8_t)-1 : (int8_t)1;
+          if (a.s_out) a.s_out[(long long)rc * n + i] = sv;
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) {
     const int i = i_base + qq;
     if (i >= n) break;
-    const float s = nmfa_update(acc[qq], __ldg(a.invn + i), __ldg(a.hn + i), z[qq], inv_t, alpha,
-                                oma, sold[qq]);
-    sn[i * Rp] = s;
-    if (extra) {
-      if (a.s_hist) a.s_hist[((long long)r * a.t_f + a.t) * n + i] = s;
-      if (a.last) {
-        a.cfg[(long long)r * n + i] = s < 0.f ? (int8_t)-1 : (int8_t)1;
-        if (a.s_out) a.s_out[(long long)r * n + i] = s;
-      }
-    }
+    if constexpr (V == 2)
+      *reinterpret_cast<float2*>(sn + i * Rp) = make_float2(acc[qq][0], acc[qq][1]);
+    else
+      sn[i * Rp] = acc[qq][0];
   }
 }
 
@@ -181,7 +250,9 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
     set_error("sparse path: needs n <= 524280 and n x padded replicas < 2^31 per plan");
     return NMFA_ERR_ARG;
   }
-  const dim3 grid((unsigned)((pl->Rp / 32 + 7) / 8), (unsigned)((p->n + 7) / 8));
+  // two replicas per lane whenever the padded replica count allows (Rp % 64 == 0)
+  const bool v2 = pl->Rp % 64 == 0;
+  const dim3 grid((unsigned)((pl->Rp / (v2 ? 64 : 32) + 7) / 8), (unsigned)((p->n + 7) / 8));
   float* cur = pl->d_sa;
   float* nxt = pl->d_sb;
   for (int t = 0; t < pl->t_f; ++t) {
@@ -190,7 +261,10 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
     a.last = (t == pl->t_f - 1);
     a.s_old = cur;
     a.s_new = nxt;
-    sparse_step_kernel<<<grid, 256, 0, st>>>(a);
+    if (v2)
+      sparse_step_kernel<2><<<grid, 256, 0, st>>>(a);
+    else
+      sparse_step_kernel<1><<<grid, 256, 0, st>>>(a);
     NMFA_LAUNCH_CHECK();
     std::swap(cur, nxt);
   }
