@@ -594,6 +594,11 @@ def main():
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="sk65536: fused peer-store exchange (default) or NCCL all-gather")
     args = ap.parse_args()
+    if args.impl != "reference":
+        # the CUDA library ships prebuilt with the snapshot; build it if it is
+        # missing or stale (no-op otherwise)
+        from paper_1806_08422_b200 import build as _nbuild
+        _nbuild.build()
     if args.workload == "ground26":
         run_ground(args, args.impl)
         return
