@@ -32,15 +32,15 @@ def build(force=False, verbose=False):
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
     extra = os.environ.get("NMFA_NVCC_DEFS", "").split()   # experiment builds only
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", OUT + ".tmp",
-           *sources()]
+    tmp = f"{OUT}.{os.getpid()}.tmp"  # per process: concurrent ranks may build at once
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", tmp, *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libnmfa_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(tmp, OUT)  # atomic: a loader sees the old or the new library, never a partial one
     return OUT
 
 
