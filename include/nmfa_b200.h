@@ -61,6 +61,16 @@ typedef struct {
 int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* edges_i_host,
                         const int64_t* edges_j_host, const double* weights_host,
                         const double* h_host, int32_t device, nmfa_problem_t** out);
+/* The same problem from a dense row-major n x n coupling matrix (symmetric,
+ * zero diagonal; the `J` that kernels.anneal_dense receives, solver.py:206-210,
+ * problem.py:100-104); h_host may be NULL. */
+int nmfa_problem_create_dense(int64_t n, const double* J_host, const double* h_host,
+                              int32_t device, nmfa_problem_t** out);
+/* A complete +-1 graph (SK) from packed sign bits: bit (i*n + j) of the
+ * row-major bitmap (word b>>5, bit b&31) set -> J_ij = +1, clear -> -1, read
+ * for i < j (1/64 of a float64 J). */
+int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits_host, const double* h_host,
+                                   int32_t device, nmfa_problem_t** out);
 int nmfa_problem_destroy(nmfa_problem_t* p);
 int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info);
 /* Synthetic Sherrington-Kirkpatrick instance generated ON DEVICE (BASELINE

@@ -298,6 +298,53 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
   NMFA_API_END
 }
 
+int nmfa_problem_create_dense(int64_t n, const double* J, const double* h, int32_t device,
+                              nmfa_problem_t** out) {
+  NMFA_API_BEGIN
+  if (!out || !J) return arg_error("NULL argument");
+  *out = nullptr;
+  if (n < 1) return arg_error("spin count must be positive, got " + std::to_string(n));
+  if (n > (int64_t)1 << 20) return arg_error("spin count too large for a dense matrix");
+  std::vector<int64_t> ei, ej;
+  std::vector<double> w;
+  for (int64_t i = 0; i < n; ++i) {
+    if (J[i * n + i] != 0.0) return arg_error("self-couplings are not allowed");
+    for (int64_t j = i + 1; j < n; ++j) {
+      const double a = J[i * n + j];
+      if (a != J[j * n + i]) return arg_error("J must be symmetric");
+      if (a != 0.0) {
+        ei.push_back(i);
+        ej.push_back(j);
+        w.push_back(a);
+      }
+    }
+  }
+  return nmfa_problem_create(n, (int64_t)w.size(), ei.data(), ej.data(), w.data(), h, device, out);
+  NMFA_API_END
+}
+
+int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits, const double* h,
+                                   int32_t device, nmfa_problem_t** out) {
+  NMFA_API_BEGIN
+  if (!out || !sign_bits) return arg_error("NULL argument");
+  *out = nullptr;
+  if (n < 2) return arg_error("a complete +-1 graph needs n >= 2, got " + std::to_string(n));
+  if (n > (int64_t)1 << 17) return arg_error("spin count too large for the host edge list");
+  const int64_t m = n * (n - 1) / 2;
+  std::vector<int64_t> ei((size_t)m), ej((size_t)m);
+  std::vector<double> w((size_t)m);
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j, ++k) {
+      const uint64_t b = (uint64_t)i * (uint64_t)n + (uint64_t)j;  // row-major bit (i, j), i < j
+      ei[k] = i;
+      ej[k] = j;
+      w[k] = ((sign_bits[b >> 5] >> (b & 31)) & 1u) ? 1.0 : -1.0;
+    }
+  return nmfa_problem_create(n, m, ei.data(), ej.data(), w.data(), h, device, out);
+  NMFA_API_END
+}
+
 int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int64_t row_hi,
                                   int32_t device, nmfa_problem_t** out) {
   NMFA_API_BEGIN

@@ -368,3 +368,42 @@ def test_host_entry_is_thread_safe():
         t.join()
     for (wc, we), (gc, ge) in zip(want, got):
         assert np.array_equal(wc, gc) and np.array_equal(we, ge)
+
+
+def test_dense_and_bit_constructors_equal_edge_list():
+    """nmfa_problem_create_dense / _dense_bits build the same problem as the
+    edge list: same info and bit-identical anneals (plan_run on each handle)."""
+    import ctypes
+
+    from paper_1806_08422_b200 import _native
+    lib = _native.load()
+    n = 300
+    p = nb.gen_sk(n, 6)
+    J = np.zeros((n, n))
+    J[p.edges_i, p.edges_j] = p.edge_weights
+    J = J + J.T
+    bits = np.zeros((n * n + 31) // 32, np.uint32)
+    for i, j, w in zip(p.edges_i, p.edges_j, p.edge_weights):
+        if w > 0:
+            b = int(i) * n + int(j)
+            bits[b >> 5] |= np.uint32(1 << (b & 31))
+    hd, hb = ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(lib.nmfa_problem_create_dense(n, _native.ptr(np.ascontiguousarray(J)), None, 0,
+                                                ctypes.byref(hd)))
+    _native.check(lib.nmfa_problem_create_dense_bits(n, _native.ptr(bits), None, 0, ctypes.byref(hb)))
+    params = nb.NmfaParams(t_f=80, seed=2)
+    temps = np.ascontiguousarray(params.schedule.temperatures(params.t_f))
+    outs = []
+    for h in (p.device_handle().handle, hd, hb):
+        cfg = torch.empty((256, n), dtype=torch.int8, device="cuda")
+        e = torch.empty(256, dtype=torch.float64, device="cuda")
+        _native.check(lib.nmfa_anneal(h, 256, params.t_f, _native.ptr(temps), params.alpha,
+                                      params.sigma, params.seed, 0, None, None, _native.ptr(cfg),
+                                      _native.ptr(e), None, None, None, None))
+        outs.append((cfg, e))
+    for cfg, e in outs[1:]:
+        assert torch.equal(cfg, outs[0][0]) and torch.equal(e, outs[0][1])
+    lib.nmfa_problem_destroy(hd)
+    lib.nmfa_problem_destroy(hb)
+    bad = np.eye(3)
+    assert lib.nmfa_problem_create_dense(3, _native.ptr(bad), None, 0, ctypes.byref(hd)) == 1
