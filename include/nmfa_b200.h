@@ -66,6 +66,12 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* edges_i_host,
  * problem.py:100-104); h_host may be NULL. */
 int nmfa_problem_create_dense(int64_t n, const double* J_host, const double* h_host,
                               int32_t device, nmfa_problem_t** out);
+/* ... or from the symmetric CSR that kernels.anneal_sparse receives
+ * (problem.py:78-88; indptr[n+1], indices/weights[indptr[n]]): entries with
+ * j > i define the couplers, and their mirror entries must be present. */
+int nmfa_problem_create_csr(int64_t n, const int64_t* indptr, const int64_t* indices,
+                            const double* weights, const double* h_host, int32_t device,
+                            nmfa_problem_t** out);
 /* A complete +-1 graph (SK) from packed sign bits: bit (i*n + j) of the
  * row-major bitmap (word b>>5, bit b&31) set -> J_ij = +1, clear -> -1, read
  * for i < j (1/64 of a float64 J). */

@@ -26,6 +26,7 @@ SIGNATURES = {
     "nmfa_problem_destroy": (_i32, [_p]),
     "nmfa_problem_create_dense": (_i32, [_i64, _p, _p, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_create_dense_bits": (_i32, [_i64, _p, _p, _i32, ctypes.POINTER(_p)]),
+    "nmfa_problem_create_csr": (_i32, [_i64, _p, _p, _p, _p, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_get_info": (_i32, [_p, _p]),
     "nmfa_problem_set_path": (_i32, [_p, _i32]),
     "nmfa_plan_create": (_i32, [_p, _i64, _i32, _p, _f64, _f64, ctypes.POINTER(_p)]),

@@ -323,6 +323,38 @@ int nmfa_problem_create_dense(int64_t n, const double* J, const double* h, int32
   NMFA_API_END
 }
 
+int nmfa_problem_create_csr(int64_t n, const int64_t* indptr, const int64_t* indices,
+                            const double* weights, const double* h, int32_t device,
+                            nmfa_problem_t** out) {
+  NMFA_API_BEGIN
+  if (!out || !indptr || !indices || !weights) return arg_error("NULL argument");
+  *out = nullptr;
+  if (n < 1) return arg_error("spin count must be positive, got " + std::to_string(n));
+  if (indptr[0] != 0) return arg_error("indptr must start at 0");
+  std::vector<int64_t> ei, ej;
+  std::vector<double> w;
+  int64_t lower = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (indptr[i + 1] < indptr[i]) return arg_error("indptr must be nondecreasing");
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int64_t j = indices[k];
+      if (j < 0 || j >= n) return arg_error("coupler index out of range [0, " + std::to_string(n) + ")");
+      if (j > i) {
+        ei.push_back(i);
+        ej.push_back(j);
+        w.push_back(weights[k]);
+      } else if (j < i) {
+        ++lower;
+      } else {
+        return arg_error("self-couplings are not allowed");
+      }
+    }
+  }
+  if (lower != (int64_t)w.size()) return arg_error("the CSR must be symmetric (problem.py:78-88)");
+  return nmfa_problem_create(n, (int64_t)w.size(), ei.data(), ej.data(), w.data(), h, device, out);
+  NMFA_API_END
+}
+
 int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits, const double* h,
                                    int32_t device, nmfa_problem_t** out) {
   NMFA_API_BEGIN

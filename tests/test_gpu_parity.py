@@ -391,10 +391,15 @@ def test_dense_and_bit_constructors_equal_edge_list():
     _native.check(lib.nmfa_problem_create_dense(n, _native.ptr(np.ascontiguousarray(J)), None, 0,
                                                 ctypes.byref(hd)))
     _native.check(lib.nmfa_problem_create_dense_bits(n, _native.ptr(bits), None, 0, ctypes.byref(hb)))
+    hc = ctypes.c_void_p()
+    ip, ix, wx = (np.ascontiguousarray(p.csr_indptr, np.int64), np.ascontiguousarray(p.csr_indices, np.int64),
+                  np.ascontiguousarray(p.csr_weights, np.float64))
+    _native.check(lib.nmfa_problem_create_csr(n, _native.ptr(ip), _native.ptr(ix), _native.ptr(wx), None,
+                                              0, ctypes.byref(hc)))
     params = nb.NmfaParams(t_f=80, seed=2)
     temps = np.ascontiguousarray(params.schedule.temperatures(params.t_f))
     outs = []
-    for h in (p.device_handle().handle, hd, hb):
+    for h in (p.device_handle().handle, hd, hb, hc):
         cfg = torch.empty((256, n), dtype=torch.int8, device="cuda")
         e = torch.empty(256, dtype=torch.float64, device="cuda")
         _native.check(lib.nmfa_anneal(h, 256, params.t_f, _native.ptr(temps), params.alpha,
@@ -405,5 +410,6 @@ def test_dense_and_bit_constructors_equal_edge_list():
         assert torch.equal(cfg, outs[0][0]) and torch.equal(e, outs[0][1])
     lib.nmfa_problem_destroy(hd)
     lib.nmfa_problem_destroy(hb)
+    lib.nmfa_problem_destroy(hc)
     bad = np.eye(3)
     assert lib.nmfa_problem_create_dense(3, _native.ptr(bad), None, 0, ctypes.byref(hd)) == 1
