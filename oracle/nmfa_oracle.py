@@ -354,66 +354,66 @@ TIE_TOL = 1e-9
 
 
 def gray_ground(problem, chunk_bits=16):
+    """Minimum energy over all 2^n configurations and its multiplicity within
+    TIE_TOL (the semantics of _kernels_numpy.py:64-87), enumerated chunk by
+    chunk in configuration-index order: configuration k sets s_i = -1 where bit
+    i of k is set, and its energy is summed over the canonical edge list."""
     n = problem.n
-    J = np.zeros((n, n))
-    J[problem.edges_i, problem.edges_j] = problem.edge_weights
-    J = J + J.T
+    ei, ej = np.asarray(problem.edges_i), np.asarray(problem.edges_j)
+    w = np.asarray(problem.edge_weights, dtype=np.float64)
     h = np.asarray(problem.h, dtype=np.float64)
-    shifts = np.arange(n, dtype=np.uint64)
-    total = 1 << n
-    chunk = min(total, 1 << chunk_bits)
-    emin, count = np.inf, 0
-    for start in range(0, total, chunk):
-        ks = np.arange(start, min(start + chunk, total), dtype=np.uint64)
-        S = 1.0 - 2.0 * ((ks[:, None] >> shifts[None, :]) & np.uint64(1))
-        E = 0.5 * np.einsum("bi,bi->b", S @ J, S) + S @ h
-        cmin = float(E.min())
-        if cmin < emin - TIE_TOL:
-            emin = cmin
-            count = int(np.count_nonzero(E <= emin + TIE_TOL))
+    bit = np.uint64(1) << np.arange(n, dtype=np.uint64)
+    best, ties = np.inf, 0
+    step = 1 << min(n, chunk_bits)
+    for first in range(0, 1 << n, step):
+        k = np.arange(first, min(first + step, 1 << n), dtype=np.uint64)
+        spins = np.where((k[:, None] & bit[None, :]) != 0, -1.0, 1.0)
+        e = (spins[:, ei] * spins[:, ej]) @ w + spins @ h
+        low = float(e.min())
+        if low < best - TIE_TOL:  # a new minimum resets the count
+            best = low
+            ties = int(np.count_nonzero(e <= best + TIE_TOL))
         else:
-            count += int(np.count_nonzero(E <= emin + TIE_TOL))
-    return emin, count
+            ties += int(np.count_nonzero(e <= best + TIE_TOL))
+    return best, ties
 
 
 def gray_ground_fast(problem):
-    """numba restatement of the reference's sequential Gray walk
-    (_kernels_numba.py:83-114): the CPU baseline for the enumerator."""
+    """CPU baseline for the enumerator: the reference's sequential Gray-code walk
+    (_kernels_numba.py:83-114) jitted with numba -- one spin flip per step, the
+    flipped spin's field summed over its CSR row, ties within 1e-9."""
     from numba import njit
 
     global _gray_jit
     if "_gray_jit" not in globals():
         @njit(cache=False, nogil=True)
-        def _gray(indptr, indices, weights, h):
-            n = h.shape[0]
-            s = np.full(n, -1.0)
-            e = 0.0
-            for i in range(n):
-                for k in range(indptr[i], indptr[i + 1]):
-                    j = indices[k]
-                    if j > i:
-                        e += weights[k] * s[i] * s[j]
-                e += h[i] * s[i]
-            emin = e
-            count = 1
-            total = np.int64(1) << n
-            for step in range(1, total):
-                v = 0
-                k = step
-                while k & 1 == 0:
-                    k >>= 1
-                    v += 1
-                s[v] = -s[v]
-                acc = 0.0
-                for k in range(indptr[v], indptr[v + 1]):
-                    acc += weights[k] * s[indices[k]]
-                e += 2.0 * s[v] * (h[v] + acc)
-                if e < emin - 1e-9:
-                    emin = e
-                    count = 1
-                elif e <= emin + 1e-9:
-                    count += 1
-            return emin, count
-        _gray_jit = _gray
+        def _walk(ptr, col, val, field):
+            n = field.shape[0]
+            spin = -np.ones(n)
+            # E(all -1) = sum_{i<j} w + sum_i -h_i
+            energy = 0.0
+            for a in range(n):
+                for q in range(ptr[a], ptr[a + 1]):
+                    if col[q] > a:
+                        energy += val[q]
+                energy -= field[a]
+            best, ties = energy, 1
+            for code in range(1, np.int64(1) << n):
+                flip = 0  # index of the lowest set bit of `code`
+                c = code
+                while (c & 1) == 0:
+                    c >>= 1
+                    flip += 1
+                spin[flip] = -spin[flip]
+                local = field[flip]
+                for q in range(ptr[flip], ptr[flip + 1]):
+                    local += val[q] * spin[col[q]]
+                energy += 2.0 * spin[flip] * local
+                if energy < best - 1e-9:
+                    best, ties = energy, 1
+                elif energy <= best + 1e-9:
+                    ties += 1
+            return best, ties
+        _gray_jit = _walk
     return _gray_jit(problem.csr_indptr, problem.csr_indices, problem.csr_weights,
                      np.asarray(problem.h, dtype=np.float64))
