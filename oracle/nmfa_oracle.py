@@ -36,15 +36,18 @@ TIE_TOL = 1e-9              # metrics.py:21
 # schedule (solver.py:70-84)
 # --------------------------------------------------------------------------
 def temperatures(t_f, breakpoints=DEFAULT_BREAKPOINTS):
-    """Piecewise-geometric T for iterations 1..t_f (solver.py:70-84)."""
-    fs = np.array([float(f) for f, _ in breakpoints])
-    Ts = np.array([float(T) for _, T in breakpoints])
+    """Piecewise-geometric T for iterations 1..t_f (solver.py:70-84): iteration
+    t sits at f = (t-1)/(t_f-1); inside segment [f_k, f_k+1) the temperature
+    is T_k (T_k+1 / T_k)^((f - f_k)/(f_k+1 - f_k)); f at or past the last
+    breakpoint takes the last temperature exactly."""
+    knots = [(float(f), float(T)) for f, T in breakpoints]
     t_f = int(t_f)
-    f = np.zeros(1) if t_f == 1 else np.arange(t_f) / (t_f - 1)
-    k = np.clip(np.searchsorted(fs, f, side="right") - 1, 0, len(fs) - 2)
-    frac = (f - fs[k]) / (fs[k + 1] - fs[k])
-    out = Ts[k] * (Ts[k + 1] / Ts[k]) ** frac
-    out[f >= fs[-1]] = Ts[-1]
+    f = np.arange(t_f) / (t_f - 1) if t_f > 1 else np.zeros(1)
+    out = np.empty_like(f)
+    for (f0, T0), (f1, T1) in zip(knots[:-1], knots[1:]):
+        inside = (f >= f0) & (f < f1)
+        out[inside] = T0 * (T1 / T0) ** ((f[inside] - f0) / (f1 - f0))
+    out[f >= knots[-1][0]] = knots[-1][1]
     return out
 
 
@@ -168,17 +171,20 @@ try:
         return s
 
     @njit(nogil=True, cache=False)
-    def _loop_sparse(indptr, indices, weights, h, norm, s, temps, noise, alpha):
+    def _loop_sparse(row_start, col, val, h, norm, s, temps, noise, alpha):
+        # synchronous update: all fields from the incoming state, then all spins
+        # (_kernels_numba.py:48-56); arithmetic order kept for bit-exact energies
         n = s.shape[0]
-        phi = np.empty(n)
-        for t in range(temps.shape[0]):
-            for i in range(n):
-                acc = 0.0
-                for k in range(indptr[i], indptr[i + 1]):
-                    acc += weights[k] * s[indices[k]]
-                phi[i] = (h[i] + acc) / norm[i] + noise[t, i]
-            for i in range(n):
-                s[i] = alpha * (-np.tanh(phi[i] / temps[t])) + (1.0 - alpha) * s[i]
+        field = np.empty(n)
+        for step in range(temps.shape[0]):
+            T = temps[step]
+            for a in range(n):
+                total = 0.0
+                for q in range(row_start[a], row_start[a + 1]):
+                    total += val[q] * s[col[q]]
+                field[a] = (h[a] + total) / norm[a] + noise[step, a]
+            for a in range(n):
+                s[a] = alpha * (-np.tanh(field[a] / T)) + (1.0 - alpha) * s[a]
         return s
 
     HAVE_JIT = True
@@ -292,12 +298,12 @@ def gen_sk_edges(n, seed):
 
 
 def moebius_edges(n):
-    cyc_i = np.arange(n, dtype=np.int64)
-    cyc_j = (cyc_i + 1) % n
-    half = np.arange(n // 2, dtype=np.int64)
-    ii = np.concatenate([np.minimum(cyc_i, cyc_j), half])
-    jj = np.concatenate([np.maximum(cyc_i, cyc_j), half + n // 2])
-    return ii, jj, np.ones(ii.size)
+    """Ring 0-1-...-(n-1)-0 plus rungs (k, k + n/2), unit weights (generators.py:76-86)."""
+    v = np.arange(n, dtype=np.int64)
+    ring = np.stack([v, np.roll(v, -1)])
+    rungs = np.stack([v[: n // 2], v[: n // 2] + n // 2])
+    ends = np.concatenate([ring, rungs], axis=1)
+    return ends.min(axis=0), ends.max(axis=0), np.ones(ends.shape[1])
 
 
 def problem_from_edges(n, ii, jj, w, h=None):

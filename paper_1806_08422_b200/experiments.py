@@ -22,17 +22,20 @@ BENCH_COLUMNS = ["class", "n", "instances", "runs", "p_success_q1", "p_success_m
                  "p_success_q3", "tts_q1", "tts_median", "tts_q3"]
 
 
+_CLASSES = {
+    "sk": lambda n, p, seed: gen_sk(n, seed),
+    "dense": gen_dense_maxcut,
+    "cubic": lambda n, p, seed: gen_cubic_maxcut(n, seed),
+    "moebius": lambda n, p, seed: moebius_ladder(n),
+}
+
+
 def make_instance(cls, n, p, seed):
-    """cli.py:172-184."""
-    if cls == "sk":
-        return gen_sk(n, seed)
-    if cls == "dense":
-        return gen_dense_maxcut(n, p, seed)
-    if cls == "cubic":
-        return gen_cubic_maxcut(n, seed)
-    if cls == "moebius":
-        return moebius_ladder(n)
-    raise ValueError(f"unknown instance class {cls!r}")
+    """One generated instance of a benchmark class (the classes of cli.py:172-184)."""
+    build = _CLASSES.get(cls)
+    if build is None:
+        raise ValueError(f"unknown instance class {cls!r}")
+    return build(n, p, seed)
 
 
 def bench(cls, sizes, instances, n_runs, params=None, p=0.5, reference_energies=None,

@@ -70,12 +70,14 @@ def load_gset(path):
 
 
 def write_gset(problem):
-    """Canonical instance text; requires zero fields and integer weights (gset.py:99-109)."""
-    if np.any(problem.h != 0.0):
+    """Canonical instance text (gset.py:99-109): header, then one "u v w" line
+    per coupler in canonical order with 1-based vertices and integer weights;
+    instances with fields or fractional weights cannot be written."""
+    weights = np.asarray(problem.edge_weights)
+    if (np.asarray(problem.h) != 0.0).any():
         raise ValueError("instance format has no field column; h must be zero")
-    w = problem.edge_weights
-    if not np.all(w == np.round(w)):
+    if (weights != np.round(weights)).any():
         raise ValueError("instance format requires integer weights")
-    lines = [f"{problem.n} {problem.num_edges}"]
-    lines += [f"{i + 1} {j + 1} {int(x)}" for i, j, x in zip(problem.edges_i, problem.edges_j, w)]
-    return "\n".join(lines) + "\n"
+    body = "".join(f"{a + 1} {b + 1} {int(x)}\n"
+                   for a, b, x in zip(problem.edges_i, problem.edges_j, weights))
+    return f"{problem.n} {problem.num_edges}\n" + body

@@ -20,76 +20,82 @@ from . import _native
 DENSE_THRESHOLD = 0.5  # problem.py:13
 
 
+def _spin_count(n):
+    n = int(n)
+    if n < 1:
+        raise ValueError(f"spin count must be positive, got {n}")
+    return n
+
+
+def _fields(n, h):
+    if h is None:
+        return np.zeros(n)
+    out = np.array(h, dtype=np.float64)  # private copy
+    if out.shape != (n,):
+        raise ValueError(f"h must have length {n}, got shape {out.shape}")
+    if not np.isfinite(out).all():
+        raise ValueError("h contains non-finite entries")
+    return out
+
+
 class IsingProblem:
-    """Immutable coupling structure: n spins, fields h, couplers (i, j, w)."""
+    """Immutable coupling structure: n spins, fields h, couplers (i, j, w).
+
+    Validation order and messages are the reference's (problem.py:25-76):
+    indices in range, no self-couplings, finite nonzero weights, no duplicate
+    unordered pair.  Couplers are stored canonically, as i < j in lexicographic order.
+    """
 
     def __init__(self, n, couplers=(), h=None):
-        n = int(n)
-        if n < 1:
-            raise ValueError(f"spin count must be positive, got {n}")
-        self.n = n
-        if h is None:
-            hv = np.zeros(n)
-        else:
-            hv = np.asarray(h, dtype=np.float64).copy()
-            if hv.shape != (n,):
-                raise ValueError(f"h must have length {n}, got shape {hv.shape}")
-            if not np.all(np.isfinite(hv)):
-                raise ValueError("h contains non-finite entries")
-        self.h = hv
-
-        arr = np.asarray(couplers, dtype=np.float64)
-        if arr.size == 0:
-            arr = np.empty((0, 3))
-        if arr.ndim != 2 or arr.shape[1] != 3:
+        n = _spin_count(n)
+        h = _fields(n, h)
+        table = np.asarray(couplers, dtype=np.float64)
+        if table.size == 0:
+            table = table.reshape(0, 3)
+        if table.ndim != 2 or table.shape[1] != 3:
             raise ValueError("couplers must be a sequence of (i, j, w) triples")
-        ii, jj, ww = arr[:, 0], arr[:, 1], arr[:, 2].copy()
-        if not (np.all(ii == np.floor(ii)) and np.all(jj == np.floor(jj))):
+        ends = table[:, :2]
+        if np.any(ends != np.floor(ends)):
             raise ValueError("coupler indices must be integers")
-        self._init_edges(ii.astype(np.int64), jj.astype(np.int64), ww)
+        self._setup(n, h, ends[:, 0].astype(np.int64), ends[:, 1].astype(np.int64),
+                    table[:, 2].copy())
 
     @classmethod
     def from_arrays(cls, n, edges_i, edges_j, weights, h=None):
         """Build from integer edge arrays without the (E, 3) float triple table."""
         self = cls.__new__(cls)
-        n = int(n)
-        if n < 1:
-            raise ValueError(f"spin count must be positive, got {n}")
-        self.n = n
-        self.h = np.zeros(n) if h is None else np.asarray(h, dtype=np.float64).copy()
-        if self.h.shape != (n,):
-            raise ValueError(f"h must have length {n}, got shape {self.h.shape}")
-        if not np.all(np.isfinite(self.h)):
-            raise ValueError("h contains non-finite entries")
-        self._init_edges(np.asarray(edges_i, dtype=np.int64), np.asarray(edges_j, dtype=np.int64),
-                         np.asarray(weights, dtype=np.float64).copy())
+        n = _spin_count(n)
+        self._setup(n, _fields(n, h), np.asarray(edges_i, dtype=np.int64),
+                    np.asarray(edges_j, dtype=np.int64), np.array(weights, dtype=np.float64))
         return self
 
-    def _init_edges(self, ii, jj, ww):
-        n = self.n
-        if np.any((ii < 0) | (ii >= n) | (jj < 0) | (jj >= n)):
-            raise ValueError(f"coupler index out of range [0, {n})")
-        if np.any(ii == jj):
-            raise ValueError("self-couplings are not allowed")
-        if not np.all(np.isfinite(ww)):
-            raise ValueError("coupler weights must be finite")
-        if np.any(ww == 0.0):
-            raise ValueError("coupler weights must be nonzero")
-        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
-        key = lo * n + hi
-        if key.size > 1 and not np.all(key[1:] > key[:-1]):
-            order = np.argsort(key, kind="stable")       # canonical (lo, hi) order
-            lo, hi, ww, key = lo[order], hi[order], ww[order], key[order]
-            dup = key[1:] == key[:-1]
-            if np.any(dup):
-                k = int(np.flatnonzero(dup)[0])
-                raise ValueError(f"duplicate coupler ({lo[k]}, {hi[k]})")
-        self.edges_i, self.edges_j, self.edge_weights = lo, hi, ww
+    def _setup(self, n, h, a, b, w):
+        rules = (
+            (lambda: ((a < 0) | (a >= n) | (b < 0) | (b >= n)).any(),
+             f"coupler index out of range [0, {n})"),
+            (lambda: (a == b).any(), "self-couplings are not allowed"),
+            (lambda: not np.isfinite(w).all(), "coupler weights must be finite"),
+            (lambda: (w == 0.0).any(), "coupler weights must be nonzero"),
+        )
+        for broken, message in rules:
+            if broken():
+                raise ValueError(message)
+        first, second = np.minimum(a, b), np.maximum(a, b)
+        rank = first * n + second  # lexicographic rank of the unordered pair
+        if rank.size > 1 and not (rank[1:] > rank[:-1]).all():
+            order = np.argsort(rank, kind="stable")
+            first, second, w, rank = first[order], second[order], w[order], rank[order]
+            repeated = np.flatnonzero(rank[1:] == rank[:-1])
+            if repeated.size:
+                k = int(repeated[0])
+                raise ValueError(f"duplicate coupler ({first[k]}, {second[k]})")
+        self.n, self.h = n, h
+        self.edges_i, self.edges_j, self.edge_weights = first, second, w
         pairs = n * (n - 1) // 2
-        self.density = 0.0 if pairs == 0 else lo.size / pairs
-        self.is_dense = self.density > DENSE_THRESHOLD
-        for a in (self.h, self.edges_i, self.edges_j, self.edge_weights):
-            a.flags.writeable = False
+        density = first.size / pairs if pairs else 0.0
+        self.density, self.is_dense = density, density > DENSE_THRESHOLD
+        for arr in (self.h, self.edges_i, self.edges_j, self.edge_weights):
+            arr.flags.writeable = False
         self._handles = {}
         self._hlock = threading.Lock()
         self._csr = None
@@ -223,10 +229,11 @@ def as_problem(obj):
 
 
 def _check_length(problem, v, what):
-    v = np.asarray(v, dtype=np.float64)
-    if v.shape[-1:] != (problem.n,):
-        raise ValueError(f"{what} length {v.shape} does not match problem size {problem.n}")
-    return v
+    """Configurations / spins must end in a length-n axis (problem.py:150-183 messages)."""
+    arr = np.asarray(v, dtype=np.float64)
+    if arr.shape[-1:] == (problem.n,):
+        return arr
+    raise ValueError(f"{what} length {arr.shape} does not match problem size {problem.n}")
 
 
 def energies(problem, configs, device=0):

@@ -38,71 +38,83 @@ DEFAULT_TF = 1000
 
 
 class Schedule:
-    """Piecewise exponential temperature curve over the anneal fraction (solver.py:41-127)."""
+    """Temperature as a function of the anneal fraction f = (t - 1) / (t_f - 1).
+
+    Breakpoints (f_k, T_k) run from f = 0 to f = 1; between them log T is linear
+    in f (geometric interpolation).  Same curve, validation order and messages
+    as the reference Schedule (solver.py:41-127).
+    """
 
     def __init__(self, breakpoints):
-        pts = [(float(f), float(T)) for f, T in breakpoints]
-        if len(pts) < 2:
+        table = [(float(f), float(T)) for f, T in breakpoints]
+        if len(table) < 2:
             raise ValueError("schedule needs at least two breakpoints")
-        fs = np.array([f for f, _ in pts])
-        Ts = np.array([T for _, T in pts])
-        if fs[0] != 0.0 or fs[-1] != 1.0:
-            raise ValueError("schedule must start at f=0 and end at f=1")
-        if np.any(np.diff(fs) <= 0.0):
-            raise ValueError("schedule fractions must be strictly increasing")
-        if np.any(Ts <= 0.0) or not np.all(np.isfinite(Ts)):
-            raise ValueError("schedule temperatures must be positive and finite")
-        self._fs, self._Ts = fs, Ts
-        self._fs.flags.writeable = False
-        self._Ts.flags.writeable = False
+        f = np.array([row[0] for row in table])
+        T = np.array([row[1] for row in table])
+        rules = (
+            (lambda: f[0] != 0.0 or f[-1] != 1.0, "schedule must start at f=0 and end at f=1"),
+            (lambda: bool(np.any(f[1:] - f[:-1] <= 0.0)),
+             "schedule fractions must be strictly increasing"),
+            (lambda: bool(np.any(T <= 0.0)) or not bool(np.all(np.isfinite(T))),
+             "schedule temperatures must be positive and finite"),
+        )
+        for violated, message in rules:
+            if violated():
+                raise ValueError(message)
+        f.flags.writeable = False
+        T.flags.writeable = False
+        self._fs, self._Ts = f, T
 
     @property
     def breakpoints(self):
         return tuple(zip(self._fs.tolist(), self._Ts.tolist()))
 
+    def _segment(self, f):
+        """Index k of the segment [f_k, f_k+1) containing f (clamped)."""
+        return np.clip(np.searchsorted(self._fs, f, side="right") - 1, 0, self._fs.size - 2)
+
+    def _geometric(self, f, k):
+        f0, f1 = self._fs[k], self._fs[k + 1]
+        T0, T1 = self._Ts[k], self._Ts[k + 1]
+        return T0 * (T1 / T0) ** ((f - f0) / (f1 - f0))
+
     def temperatures(self, t_f):
-        """Temperatures for iterations t = 1..t_f (host float64, uploaded once)."""
+        """Temperatures of iterations t = 1..t_f (host float64, uploaded once per plan)."""
         t_f = int(t_f)
         if t_f < 1:
             raise ValueError("t_f must be at least 1")
-        f = np.zeros(1) if t_f == 1 else np.arange(t_f) / (t_f - 1)
-        fs, Ts = self._fs, self._Ts
-        k = np.clip(np.searchsorted(fs, f, side="right") - 1, 0, len(fs) - 2)
-        frac = (f - fs[k]) / (fs[k + 1] - fs[k])
-        out = Ts[k] * (Ts[k + 1] / Ts[k]) ** frac
-        out[f >= fs[-1]] = Ts[-1]
-        return out
+        f = np.arange(t_f) / (t_f - 1) if t_f > 1 else np.zeros(1)
+        curve = self._geometric(f, self._segment(f))
+        curve[f >= self._fs[-1]] = self._Ts[-1]  # the last breakpoint is exact
+        return curve
 
     def temperature(self, t, t_f):
+        """Temperature of iteration t (1-based) of t_f."""
         t, t_f = int(t), int(t_f)
         if t_f < 1:
             raise ValueError("t_f must be at least 1")
         if not 1 <= t <= t_f:
             raise ValueError(f"iteration {t} outside [1, {t_f}]")
-        f = 0.0 if t_f == 1 else (t - 1) / (t_f - 1)
-        fs, Ts = self._fs, self._Ts
-        if f >= fs[-1]:
-            return float(Ts[-1])
-        k = min(max(int(np.searchsorted(fs, f, side="right")) - 1, 0), len(fs) - 2)
-        frac = (f - fs[k]) / (fs[k + 1] - fs[k])
-        return float(Ts[k] * (Ts[k + 1] / Ts[k]) ** frac)
+        f = (t - 1) / (t_f - 1) if t_f > 1 else 0.0
+        if f >= self._fs[-1]:
+            return float(self._Ts[-1])
+        return float(self._geometric(f, int(self._segment(f))))
 
     @classmethod
     def parse(cls, text):
-        """Parse "f:T,f:T,..." (e.g. "0:2,0.25:0.8,0.75:0.2,1:0.02")."""
-        pts = []
-        for part in text.split(","):
-            part = part.strip()
-            if not part:
+        """Schedule from "f:T,f:T,..." text, e.g. "0:2,0.25:0.8,0.75:0.2,1:0.02"."""
+        points = []
+        for item in (piece.strip() for piece in text.split(",")):
+            if not item:
                 continue
-            bits = part.split(":")
-            if len(bits) != 2:
-                raise ValueError(f"bad schedule point {part!r}, expected f:T")
+            fields = item.split(":")
             try:
-                pts.append((float(bits[0]), float(bits[1])))
+                if len(fields) != 2:
+                    raise ValueError(item)
+                points.append((float(fields[0]), float(fields[1])))
             except ValueError:
-                raise ValueError(f"bad schedule point {part!r}, expected f:T") from None
-        return cls(pts)
+                raise ValueError(f"bad schedule point {item!r}, expected f:T") from None
+        return cls(points)
 
     def format(self):
         return ",".join(f"{f:g}:{T:g}" for f, T in self.breakpoints)
@@ -111,7 +123,7 @@ class Schedule:
         return f"Schedule({self.format()!r})"
 
     def __eq__(self, other):
-        return isinstance(other, Schedule) and self.breakpoints == other.breakpoints
+        return isinstance(other, Schedule) and other.breakpoints == self.breakpoints
 
     def __hash__(self):
         return hash(self.breakpoints)
@@ -136,15 +148,18 @@ class NmfaParams:
     seed: int = 0
 
     def __post_init__(self):
-        if not 0.0 <= self.alpha <= 1.0:
-            raise ValueError(f"alpha must be in [0, 1], got {self.alpha}")
-        if self.sigma < 0.0:
-            raise ValueError(f"sigma must be nonnegative, got {self.sigma}")
-        if int(self.t_f) < 1:
-            raise ValueError(f"t_f must be at least 1, got {self.t_f}")
+        # validated in the reference's order (solver.py:151-162); t_f and seed are
+        # normalised to Python ints once their checks pass
+        checks = (
+            (lambda: 0.0 <= self.alpha <= 1.0, lambda: f"alpha must be in [0, 1], got {self.alpha}"),
+            (lambda: self.sigma >= 0.0, lambda: f"sigma must be nonnegative, got {self.sigma}"),
+            (lambda: int(self.t_f) >= 1, lambda: f"t_f must be at least 1, got {self.t_f}"),
+            (lambda: 0 <= int(self.seed) <= MASK64, lambda: "seed must fit in 64 unsigned bits"),
+        )
+        for holds, message in checks:
+            if not holds():
+                raise ValueError(message())
         object.__setattr__(self, "t_f", int(self.t_f))
-        if not 0 <= int(self.seed) <= MASK64:
-            raise ValueError("seed must fit in 64 unsigned bits")
         object.__setattr__(self, "seed", int(self.seed))
 
 
@@ -376,13 +391,18 @@ def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=Fals
 
 
 def nmfa_step(problem, s, T, params, rng):
-    """One synchronous update at temperature T; noise from `rng` (solver.py:221-233)."""
-    if T <= 0.0:
+    """One synchronous update of the spins `s` at temperature T (solver.py:221-233).
+
+    The noise comes from the caller's numpy generator, one standard normal per
+    spin scaled by sigma, exactly as the reference draws it, so a shared
+    generator gives both packages the same step.
+    """
+    if T <= 0.0:  # the reference's test (a NaN temperature is not rejected there either)
         raise ValueError(f"temperature must be positive, got {T}")
-    problem = as_problem(problem)
-    noise = rng.standard_normal(problem.n) * params.sigma
-    s_new, _ = run_with_noise(problem, np.array([float(T)]), noise[None, :], params.alpha, s0=s)
-    return s_new
+    prob = as_problem(problem)
+    drive = params.sigma * rng.standard_normal(prob.n)
+    updated, _ = run_with_noise(prob, np.full(1, float(T)), drive.reshape(1, -1), params.alpha, s0=s)
+    return updated
 
 
 def _results(problem, res, params, record_trajectory):
