@@ -388,13 +388,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 0] = clock64();
             const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
             if (cta == 0)
+#ifdef NMFA_DBG_NOB  // timing bound only: no J bytes through TMA (results are wrong)
+              mbar_arrive_expect_tx(&full_bar[s], 2u * kATile);
+#else
               mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
+#endif
             uint8_t* st = smem + (size_t)s * kDStageBytes;
             tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb, pol_keep);
+#ifndef NMFA_DBG_NOB
             // J rows of this CTA's half of the tile: ONE box (the per-box TMA cost is
             // ~100 cycles, so the half is never split into power-of-two boxes)
             tma2d_pair(smem_u32(st + kATile), half == a.bhalf1 ? &tmB1 : &tmB0, 0,
                        (kb * a.brows + brow) * 2, fb, pol_keep);
+#endif
           }
           if (a.trace && blockIdx.x == 0 && jglob < 512)
             a.trace[jglob * 8 + 7] = wempty;  // cycles the producer waited for a free stage
