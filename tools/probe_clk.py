@@ -22,4 +22,6 @@ n1 = len(rows); proc.terminate()
 t = a.elapsed_time(b) / (4 * t_f)
 vals = [l.strip().split(",") for l in rows[n0:n1]]
 clk = statistics.median(float(v[0]) for v in vals); pw = statistics.median(float(v[1]) for v in vals)
-print(f"{sys.argv[1] if len(sys.argv)>1 else ''}: {t*1e3:.1f} us/sweep  {2*2000*2000*R/t/1e12:.0f} TFLOP/s  sm_clock {clk:.0f} MHz  power {pw:.0f} W  ({len(vals)} samples)", flush=True)
+print(f"{sys.argv[1] if len(sys.argv)>1 else ''}: {t*1e3:.1f} us/sweep  {2*2000*2000*R/(t*1e-3)/1e12:.0f} TFLOP/s  sm_clock {clk:.0f} MHz  power {pw:.0f} W  ({len(vals)} samples)", flush=True)
+import hashlib
+print(f"  cfg sha1 {hashlib.sha1(cfg.cpu().numpy().tobytes()).hexdigest()[:16]}", flush=True)
