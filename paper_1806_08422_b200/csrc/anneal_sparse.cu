@@ -7,6 +7,8 @@
 // matches the Philox counter granularity, so one Philox call per thread
 // feeds its eight spins (common.cuh noise identity).
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -22,6 +24,9 @@ struct SparseStepArgs {
   const int32_t* ptr;
   const int32_t* idx;
   const float* w;
+  const int32_t* ell_idx;  // ELL rows (problem ell_k > 0), else null
+  const float* ell_w;
+  int groups_per_warp;     // ELL kernel: consecutive spin groups per warp
   const float* invn;
   const float* hn;
   const float* s_old;
@@ -36,6 +41,62 @@ struct SparseStepArgs {
   float* s_hist;
   int last;
 };
+
+// Noise, update and stores for one warp's 8 spins (group q) x V replicas per
+// lane: the tail shared by the CSR and ELL kernels.  acc = the row sums.
+template <int V>
+__device__ __forceinline__ void sparse_finish(const SparseStepArgs& a, int q, int r,
+                                              float (&acc)[8][V], const float (&sold)[8][V]) {
+  const int n = a.n, i_base = 8 * q;
+  const int Rp = (int)a.Rp;
+  const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
+  float* __restrict__ sn = a.s_new + r;
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const int rc = r + c;
+    const bool valid = rc < a.R;
+    float z[8];
+    if (a.noise) {
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const int i = i_base + qq;
+        z[qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
+      }
+    } else {
+      const unsigned long long key = a.key_base + (unsigned long long)rc;
+      normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
+              bm_scale(a.sigma), z);
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq)
+      acc[qq][c] = nmfa_update(acc[qq][c], __ldg(a.invn + min(i_base + qq, n - 1)),
+                               __ldg(a.hn + min(i_base + qq, n - 1)), z[qq], inv_t, alpha, oma,
+                               sold[qq][c]);
+    const bool extra = valid && (a.s_hist != nullptr || a.last);
+    if (extra) {
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const int i = i_base + qq;
+        if (i >= n) break;
+        const float sv = acc[qq][c];
+        if (a.s_hist) a.s_hist[((long long)rc * a.t_f + a.t) * n + i] = sv;
+        if (a.last) {
+          a.cfg[(long long)rc * n + i] = sv < 0.f ? (int8_t)-1 : (int8_t)1;
+          if (a.s_out) a.s_out[(long long)rc * n + i] = sv;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    const int i = i_base + qq;
+    if (i >= n) break;
+    if constexpr (V == 2)
+      *reinterpret_cast<float2*>(sn + i * Rp) = make_float2(acc[qq][0], acc[qq][1]);
+    else
+      sn[i * Rp] = acc[qq][0];
+  }
+}
 
 // V replicas per lane (1 or 2): with V = 2 every state access is one float2,
 // halving the per-update address arithmetic and the uniform CSR overhead of
@@ -162,52 +223,77 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
   }
-  const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
-  float* __restrict__ sn = a.s_new + r;
-#pragma unroll
-  for (int c = 0; c < V; ++c) {
-    const int rc = r + c;
-    const bool valid = rc < a.R;
-    float z[8];
-    if (a.noise) {
-#pragma unroll
-      for (int qq = 0; qq < 8; ++qq) {
-        const int i = i_base + qq;
-        z[qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
-      }
+  sparse_finish<V>(a, q, r, acc, sold);
+}
+
+// ELL step for graphs of max degree <= K (K = 3: cubic, Moebius ladder; 4:
+// toroidal grids).  Same warp tiling, summation order and tail as the CSR
+// kernel; the fixed row length removes the row-pointer round trip, and each
+// warp walks `groups_per_warp` consecutive spin groups with the next group's
+// 8K (index, weight) slots loaded while the current group's gathers are in
+// flight, so one memory round trip per group remains on the critical path.
+template <int V, int K>
+__global__ void __launch_bounds__(256, 2) sparse_ell_kernel(const SparseStepArgs a) {
+  using Vec = typename std::conditional<V == 2, float2, float>::type;
+  static_assert(8 * K <= 32, "one slot per lane");
+  const int lane = threadIdx.x & 31;
+  const int rb = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int Rp = (int)a.Rp, n = a.n;
+  if (rb * 32 * V >= Rp) return;
+  const int r = (rb * 32 + lane) * V;
+  const float* __restrict__ so = a.s_old + r;
+  auto ld = [&](int off, float* out) {
+    const Vec x = *reinterpret_cast<const Vec*>(so + off);
+    if constexpr (V == 2) {
+      out[0] = x.x;
+      out[1] = x.y;
     } else {
-      const unsigned long long key = a.key_base + (unsigned long long)rc;
-      normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
-              bm_scale(a.sigma), z);
+      out[0] = x;
+    }
+  };
+  const int n_groups = (n + 7) / 8;
+  const int q_begin = blockIdx.y * a.groups_per_warp;
+  const int q_end = min(q_begin + a.groups_per_warp, n_groups);
+  const bool slot = lane < 8 * K;
+  int nx_idx = slot ? __ldg(a.ell_idx + q_begin * 8 * K + lane) : 0;
+  float nx_w = slot ? __ldg(a.ell_w + q_begin * 8 * K + lane) : 0.f;
+  for (int q = q_begin; q < q_end; ++q) {
+    const int off_l = nx_idx * Rp;
+    const float w_l = nx_w;
+    if (q + 1 < q_end && slot) {
+      nx_idx = __ldg(a.ell_idx + (q + 1) * 8 * K + lane);
+      nx_w = __ldg(a.ell_w + (q + 1) * 8 * K + lane);
+    }
+    const int i_base = 8 * q;
+    float sold[8][V], v[8][K][V], acc[8][V];
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      if (i_base + qq < n) {
+        ld((i_base + qq) * Rp, sold[qq]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < V; ++c) sold[qq][c] = 0.f;
+      }
     }
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq)
-      acc[qq][c] = nmfa_update(acc[qq][c], __ldg(a.invn + min(i_base + qq, n - 1)),
-                               __ldg(a.hn + min(i_base + qq, n - 1)), z[qq], inv_t, alpha, oma,
-                               sold[qq][c]);
-    const bool extra = valid && (a.s_hist != nullptr || a.last);
-    if (extra) {
 #pragma unroll
-      for (int qq = 0; qq < 8; ++qq) {
-        const int i = i_base + qq;
-        if (i >= n) break;
-        const float sv = acc[qq][c];
-        if (a.s_hist) a.s_hist[((long long)rc * a.t_f + a.t) * n + i] = sv;
-        if (a.last) {
-          a.cfg[(long long)rc * n + i] = sv < 0.f ? (int8_t)-1 : (int8_t)1;
-          if (a.s_out) a.s_out[(long long)rc * n + i] = sv;
-        }
+      for (int u = 0; u < K; ++u) ld(__shfl_sync(0xffffffffu, off_l, qq * K + u), v[qq][u]);
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      float s2[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) s2[c] = 0.f;
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        const float wv = __shfl_sync(0xffffffffu, w_l, qq * K + u);
+#pragma unroll
+        for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);  // CSR order, pads last
       }
-    }
-  }
 #pragma unroll
-  for (int qq = 0; qq < 8; ++qq) {
-    const int i = i_base + qq;
-    if (i >= n) break;
-    if constexpr (V == 2)
-      *reinterpret_cast<float2*>(sn + i * Rp) = make_float2(acc[qq][0], acc[qq][1]);
-    else
-      sn[i * Rp] = acc[qq][0];
+      for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
+    }
+    sparse_finish<V>(a, q, r, acc, sold);
   }
 }
 
@@ -217,6 +303,12 @@ __global__ void sparse_init_kernel(float* s, const float* s0, int n, long long R
   if (e >= (long long)n * Rp) return;
   const long long i = e / Rp, r = e - i * Rp;
   s[e] = (s0 && r < R) ? s0[r * n + i] : 0.f;
+}
+
+// NMFA_SPARSE_CSR=1 forces the CSR kernel on ELL-eligible graphs (A/B and tests)
+static bool ell_disabled() {
+  const char* e = getenv("NMFA_SPARSE_CSR");
+  return e && e[0] == '1';
 }
 
 int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
@@ -253,6 +345,18 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   // two replicas per lane whenever the padded replica count allows (Rp % 64 == 0)
   const bool v2 = pl->Rp % 64 == 0;
   const dim3 grid((unsigned)((pl->Rp / (v2 ? 64 : 32) + 7) / 8), (unsigned)((p->n + 7) / 8));
+  // ELL kernel: enough consecutive groups per warp to amortise the prefetch,
+  // few enough for >= 4 waves of 2 blocks per SM
+  const int ell_k = ell_disabled() ? 0 : p->ell_k;
+  const long long n_groups = (p->n + 7) / 8;
+  int sm_count = 148;
+  cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, p->device);
+  const long long want = 4LL * 2 * sm_count;
+  a.ell_idx = p->d_ell_idx;
+  a.ell_w = p->d_ell_w;
+  a.groups_per_warp =
+      (int)std::max(1LL, std::min(8LL, (long long)grid.x * n_groups / want));
+  const dim3 grid_ell(grid.x, (unsigned)((n_groups + a.groups_per_warp - 1) / a.groups_per_warp));
   float* cur = pl->d_sa;
   float* nxt = pl->d_sb;
   for (int t = 0; t < pl->t_f; ++t) {
@@ -261,7 +365,15 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
     a.last = (t == pl->t_f - 1);
     a.s_old = cur;
     a.s_new = nxt;
-    if (v2)
+    if (ell_k == 3 && v2)
+      sparse_ell_kernel<2, 3><<<grid_ell, 256, 0, st>>>(a);
+    else if (ell_k == 3)
+      sparse_ell_kernel<1, 3><<<grid_ell, 256, 0, st>>>(a);
+    else if (ell_k == 4 && v2)
+      sparse_ell_kernel<2, 4><<<grid_ell, 256, 0, st>>>(a);
+    else if (ell_k == 4)
+      sparse_ell_kernel<1, 4><<<grid_ell, 256, 0, st>>>(a);
+    else if (v2)
       sparse_step_kernel<2><<<grid, 256, 0, st>>>(a);
     else
       sparse_step_kernel<1><<<grid, 256, 0, st>>>(a);

@@ -88,7 +88,8 @@ int nmfa_problem_destroy(nmfa_problem_t* p) {
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   void* bufs[] = {p->d_invn, p->d_hn,    p->d_j_small, p->d_j_dense, p->d_csr_ptr, p->d_csr_idx,
-                  p->d_csr_w, p->d_e_i, p->d_e_j,     p->d_e_w,     p->d_h};
+                  p->d_csr_w, p->d_e_i, p->d_e_j,     p->d_e_w,     p->d_h,
+                  p->d_ell_idx, p->d_ell_w};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -253,6 +254,29 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
     if ((err = upload(&p->d_csr_ptr, ptr32.data(), ptr32.size()))) break;
     if ((err = upload(&p->d_csr_idx, cidx.data(), cidx.size()))) break;
     if ((err = upload(&p->d_csr_w, cw32.data(), cw32.size()))) break;
+    {
+      // ELL copy of the CSR rows for low-degree graphs (anneal_sparse.cu). A
+      // zero-weight pad slot leaves the row sum bit-identical: the sum starts
+      // at +0 and fmaf(0, v, s) == s for every s that can occur (never -0).
+      int64_t max_deg = 0;
+      for (int64_t i = 0; i < n; ++i) max_deg = std::max(max_deg, ptr[i + 1] - ptr[i]);
+      const int64_t n8 = (n + 7) / 8 * 8;
+      if (n > 0 && max_deg <= 4 && n8 * 4 <= INT32_MAX) {
+        const int k = max_deg <= 3 ? 3 : 4;
+        std::vector<int32_t> ei((size_t)(n8 * k));
+        std::vector<float> ew((size_t)(n8 * k), 0.f);
+        for (int64_t i = 0; i < n8; ++i)
+          for (int u = 0; u < k; ++u) {
+            const int64_t e = ptr[std::min(i, n - 1)] + u;
+            const bool real = i < n && e < ptr[i + 1];
+            ei[i * k + u] = real ? cidx[e] : (int32_t)std::min(i, n - 1);
+            ew[i * k + u] = real ? cw32[e] : 0.f;
+          }
+        if ((err = upload(&p->d_ell_idx, ei.data(), ei.size()))) break;
+        if ((err = upload(&p->d_ell_w, ew.data(), ew.size()))) break;
+        p->ell_k = k;
+      }
+    }
 
     std::vector<int32_t> e_i(n_edges), e_j(n_edges);
     for (int64_t k = 0; k < n_edges; ++k) {

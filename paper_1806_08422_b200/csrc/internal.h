@@ -65,6 +65,11 @@ struct nmfa_problem {
   int32_t* d_csr_ptr = nullptr;
   int32_t* d_csr_idx = nullptr;
   float* d_csr_w = nullptr;
+  // the same rows as ELL (max degree <= 4): ell_k slots per spin, rows padded
+  // to a multiple of 8 spins, short rows padded with (own index, weight 0)
+  int32_t ell_k = 0;
+  int32_t* d_ell_idx = nullptr;
+  float* d_ell_w = nullptr;
   // canonical upper edge list for the exact energy (problem.py:150-154)
   int32_t* d_e_i = nullptr;
   int32_t* d_e_j = nullptr;

@@ -1,0 +1,127 @@
+"""The ELL sparse kernel (graphs of max degree <= 4) against the CSR kernel.
+
+Both kernels sum each row in CSR order from +0, and the ELL pads are (own
+index, weight 0), so the two must agree BIT-EXACTLY on every graph: regular
+degree 3 and 4, mixed degrees with padded rows, isolated spins, n not a
+multiple of 8, one or two replicas per lane, injected and in-kernel noise,
+trajectories. NMFA_SPARSE_CSR=1 forces the CSR kernel (anneal_sparse.cu).
+The CSR kernel itself is pinned to the oracle by test_gpu_parity.py.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import nmfa_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1806_08422_b200 as nb  # noqa: E402
+from paper_1806_08422_b200 import _native  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1806_08422_b200 import build
+    build.build()
+    _native.load()
+
+
+def torus(rows, cols):
+    """2-D toroidal grid (G-set's degree-4 class), +-1 couplers."""
+    v = np.arange(rows * cols).reshape(rows, cols)
+    a = np.concatenate([v.ravel(), v.ravel()])
+    b = np.concatenate([np.roll(v, -1, 1).ravel(), np.roll(v, -1, 0).ravel()])
+    w = np.where(np.random.default_rng(rows * cols).random(a.size) < 0.5, 1.0, -1.0)
+    return nb.IsingProblem.from_arrays(rows * cols, np.minimum(a, b), np.maximum(a, b), w)
+
+
+def mixed(n, seed, h=False):
+    """Random graph of max degree 3 with degree-0/1/2 spins and real weights."""
+    rng = np.random.default_rng(seed)
+    deg = np.zeros(n, dtype=int)
+    pairs = set()
+    for _ in range(n):
+        i, j = rng.integers(0, n, 2)
+        if i != j and deg[i] < 3 and deg[j] < 3 and (min(i, j), max(i, j)) not in pairs:
+            pairs.add((min(i, j), max(i, j)))
+            deg[i] += 1
+            deg[j] += 1
+    e = np.array(sorted(pairs))
+    hv = rng.normal(size=n) if h else None
+    return nb.IsingProblem.from_arrays(n, e[:, 0], e[:, 1], rng.normal(size=len(e)), hv)
+
+
+GRAPHS = {
+    "moebius_1000": lambda: nb.moebius_ladder(1000),
+    "cubic_302": lambda: nb.gen_cubic_maxcut(302, 4),
+    "torus_13x11": lambda: torus(13, 11),
+    "mixed_301_h": lambda: mixed(301, 7, h=True),
+    "mixed_77": lambda: mixed(77, 3),
+}
+
+
+def _both(fn):
+    old = os.environ.get("NMFA_SPARSE_CSR")
+    try:
+        os.environ["NMFA_SPARSE_CSR"] = "1"
+        csr = fn()
+        os.environ["NMFA_SPARSE_CSR"] = "0"
+        ell = fn()
+    finally:
+        if old is None:
+            os.environ.pop("NMFA_SPARSE_CSR", None)
+        else:
+            os.environ["NMFA_SPARSE_CSR"] = old
+    return csr, ell
+
+
+@pytest.mark.parametrize("graph", sorted(GRAPHS))
+@pytest.mark.parametrize("R", [1, 37, 64, 300])
+def test_ell_equals_csr_seeded(graph, R):
+    p = GRAPHS[graph]()
+    p.device_handle().set_path("sparse")
+    params = nb.NmfaParams(t_f=60, seed=11)
+
+    def run():
+        res = nb.sample(p, params, R)
+        return res.configs.cpu().numpy(), res.energies.cpu().numpy()
+
+    (c0, e0), (c1, e1) = _both(run)
+    assert np.array_equal(c0, c1) and np.array_equal(e0, e1)
+
+
+@pytest.mark.parametrize("graph", sorted(GRAPHS))
+def test_ell_equals_csr_injected_trajectory(graph):
+    p = GRAPHS[graph]()
+    p.device_handle().set_path("sparse")
+    t_f, R = 25, 5
+    temps = O.temperatures(t_f)
+    noise = np.random.default_rng(1).standard_normal((R, t_f, p.n)) * 0.15
+
+    def run():
+        s, trs = nb.run_with_noise(p, temps, noise, 0.15, record_trajectory=True)
+        return s, np.stack([tr.spins for tr in trs])
+
+    (s0, h0), (s1, h1) = _both(run)
+    assert np.array_equal(s0, s1) and np.array_equal(h0, h1)
+
+
+def test_ell_torus_matches_oracle():
+    """Degree-4 ELL rows against the float64 oracle under injected noise."""
+    p = torus(16, 9)
+    p.device_handle().set_path("sparse")
+    t_f, R = 40, 33
+    temps = O.temperatures(t_f)
+    noise = np.random.default_rng(2).standard_normal((R, t_f, p.n)) * 0.15
+    S, _ = nb.run_with_noise(p, temps, noise, 0.15)
+    op = O.problem_from_edges(p.n, p.edges_i, p.edges_j, p.edge_weights)
+    ref = np.stack([O.anneal(op, np.zeros(p.n), temps, noise[r], 0.15)[0] for r in range(R)])
+    assert np.abs(S - ref).max() <= 2e-2
+    firm = np.abs(ref) > 2e-2
+    assert np.array_equal(np.sign(S[firm]), np.sign(ref[firm]))
