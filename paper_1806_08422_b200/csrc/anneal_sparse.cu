@@ -14,6 +14,9 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef NMFA_ELL_MINB
+#define NMFA_ELL_MINB 2  // ELL kernel blocks per SM (128 registers, no spill at V = 2)
+#endif
 #ifndef NMFA_SPARSE_MINB
 #define NMFA_SPARSE_MINB 4  // blocks per SM the register budget targets
 #endif
@@ -27,6 +30,7 @@ struct SparseStepArgs {
   const int32_t* ell_idx;  // ELL rows (problem ell_k > 0), else null
   const float* ell_w;
   int groups_per_warp;     // ELL kernel: consecutive spin groups per warp
+  int slices_per_block;    // ELL kernel: replica slices per block (1, 2, 4, 8)
   const float* invn;
   const float* hn;
   const float* s_old;
@@ -233,14 +237,20 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
 // 8K (index, weight) slots loaded while the current group's gathers are in
 // flight, so one memory round trip per group remains on the critical path.
 template <int V, int K>
-__global__ void __launch_bounds__(256, 2) sparse_ell_kernel(const SparseStepArgs a) {
+__global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const SparseStepArgs a) {
   using Vec = typename std::conditional<V == 2, float2, float>::type;
   static_assert(8 * K <= 32, "one slot per lane");
-  const int lane = threadIdx.x & 31;
-  const int rb = blockIdx.x * 8 + (threadIdx.x >> 5);
+  // grid (spin strips, replica slices), strips fastest.  A block's 8 warps
+  // cover `slices_per_block` (RS) replica slices of 32V x 8/RS strips of G
+  // groups.  Small RS keeps the resident blocks on few replica slices, so the
+  // gathered rows (n x 32V x 4 B per slice) stay in L2 (random graphs); larger
+  // RS reads wider contiguous row segments (local graphs).  profiles/r01/ell_ab*.log
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Rp = (int)a.Rp, n = a.n;
-  if (rb * 32 * V >= Rp) return;
-  const int r = (rb * 32 + lane) * V;
+  const int RS = a.slices_per_block;
+  const int slice = blockIdx.y * RS + warp % RS;
+  if (slice * 32 * V >= Rp) return;
+  const int r = (slice * 32 + lane) * V;
   const float* __restrict__ so = a.s_old + r;
   auto ld = [&](int off, float* out) {
     const Vec x = *reinterpret_cast<const Vec*>(so + off);
@@ -252,7 +262,8 @@ __global__ void __launch_bounds__(256, 2) sparse_ell_kernel(const SparseStepArgs
     }
   };
   const int n_groups = (n + 7) / 8;
-  const int q_begin = blockIdx.y * a.groups_per_warp;
+  const int q_begin = (blockIdx.x * (8 / RS) + warp / RS) * a.groups_per_warp;
+  if (q_begin >= n_groups) return;
   const int q_end = min(q_begin + a.groups_per_warp, n_groups);
   const bool slot = lane < 8 * K;
   int nx_idx = slot ? __ldg(a.ell_idx + q_begin * 8 * K + lane) : 0;
@@ -305,6 +316,8 @@ __global__ void sparse_init_kernel(float* s, const float* s0, int n, long long R
   s[e] = (s0 && r < R) ? s0[r * n + i] : 0.f;
 }
 
+constexpr int kEllSlicesPerBlock = 1;
+
 // NMFA_SPARSE_CSR=1 forces the CSR kernel on ELL-eligible graphs (A/B and tests)
 static bool ell_disabled() {
   const char* e = getenv("NMFA_SPARSE_CSR");
@@ -343,20 +356,31 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
     return NMFA_ERR_ARG;
   }
   // two replicas per lane whenever the padded replica count allows (Rp % 64 == 0)
-  const bool v2 = pl->Rp % 64 == 0;
+  const char* v_env = getenv("NMFA_SPARSE_V");  // A/B: "1" forces one replica per lane
+  const bool v2 = pl->Rp % 64 == 0 && !(v_env && v_env[0] == '1');
   const dim3 grid((unsigned)((pl->Rp / (v2 ? 64 : 32) + 7) / 8), (unsigned)((p->n + 7) / 8));
-  // ELL kernel: enough consecutive groups per warp to amortise the prefetch,
-  // few enough for >= 4 waves of 2 blocks per SM
+  // ELL kernel: G consecutive groups per warp amortise the slot prefetch; G
+  // is capped so that the resident blocks (2 per SM) still span few replica
+  // slices (the L2-resident working set)
   const int ell_k = ell_disabled() ? 0 : p->ell_k;
   const long long n_groups = (p->n + 7) / 8;
+  const long long n_slices = pl->Rp / (v2 ? 64 : 32);
   int sm_count = 148;
   cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, p->device);
-  const long long want = 4LL * 2 * sm_count;
   a.ell_idx = p->d_ell_idx;
   a.ell_w = p->d_ell_w;
-  a.groups_per_warp =
-      (int)std::max(1LL, std::min(8LL, (long long)grid.x * n_groups / want));
-  const dim3 grid_ell(grid.x, (unsigned)((n_groups + a.groups_per_warp - 1) / a.groups_per_warp));
+  a.slices_per_block = kEllSlicesPerBlock;
+  if (const char* e = getenv("NMFA_ELL_RS")) a.slices_per_block = atoi(e);
+  if (a.slices_per_block != 1 && a.slices_per_block != 2 && a.slices_per_block != 4 &&
+      a.slices_per_block != 8)
+    a.slices_per_block = kEllSlicesPerBlock;
+  const int strips_per_block = 8 / a.slices_per_block;
+  a.groups_per_warp = (int)std::max(
+      1LL, std::min(8LL, n_groups * a.slices_per_block / (8LL * 2 * sm_count)));
+  if (const char* e = getenv("NMFA_ELL_G")) a.groups_per_warp = std::max(1, atoi(e));
+  const long long strips = (n_groups + a.groups_per_warp - 1) / a.groups_per_warp;
+  const dim3 grid_ell((unsigned)((strips + strips_per_block - 1) / strips_per_block),
+                      (unsigned)((n_slices + a.slices_per_block - 1) / a.slices_per_block));
   float* cur = pl->d_sa;
   float* nxt = pl->d_sb;
   for (int t = 0; t < pl->t_f; ++t) {

@@ -1,6 +1,8 @@
-# ncu --set full of the V=2 CSR kernel on moebius_ladder(131072), R=1024 (one launch)
+# ncu --set full of the sparse kernel (ELL when max degree <= 4) on moebius_ladder(131072), R=1024 (one launch)
+# usage: bash tools/ncu_sparse.sh [tag] [extra env assignments...]
 set -e
 mkdir -p gpurun_out
-timeout 300 python tools/prof_sparse_one.py
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_step_kernel -s 2 -c 1 \
-  -o gpurun_out/sparse_v2 -f python tools/prof_sparse_one.py > gpurun_out/ncu_sparse.log 2>&1
+tag=${1:-sparse_ell}; shift || true
+env "$@" timeout 300 python tools/prof_sparse_one.py ${PROF_GRAPH:-moebius}
+env "$@" timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_ -s 2 -c 1 \
+  -o gpurun_out/$tag -f python tools/prof_sparse_one.py ${PROF_GRAPH:-moebius} > gpurun_out/ncu_$tag.log 2>&1
