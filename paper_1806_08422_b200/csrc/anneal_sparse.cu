@@ -46,35 +46,54 @@ struct SparseStepArgs {
   int last;
 };
 
-// Noise, update and stores for one warp's 8 spins (group q) x V replicas per
-// lane: the tail shared by the CSR and ELL kernels.  acc = the row sums.
+// The N(0, sigma^2) noise of one warp's 8 spins (group q) x V replicas per
+// lane: injected (`a.noise`) or in-kernel Philox.  Independent of the state,
+// so the ELL kernel computes it while the group's gathers are in flight.
 template <int V>
-__device__ __forceinline__ void sparse_finish(const SparseStepArgs& a, int q, int r,
-                                              float (&acc)[8][V], const float (&sold)[8][V]) {
+__device__ __forceinline__ void sparse_noise(const SparseStepArgs& a, int q, int r,
+                                             float (&z)[V][8]) {
   const int n = a.n, i_base = 8 * q;
-  const int Rp = (int)a.Rp;
-  const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
-  float* __restrict__ sn = a.s_new + r;
 #pragma unroll
   for (int c = 0; c < V; ++c) {
     const int rc = r + c;
-    const bool valid = rc < a.R;
-    float z[8];
     if (a.noise) {
+      const bool valid = rc < a.R;
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
         const int i = i_base + qq;
-        z[qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
+        z[c][qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
       }
     } else {
       const unsigned long long key = a.key_base + (unsigned long long)rc;
       normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
-              bm_scale(a.sigma), z);
+              bm_scale(a.sigma), z[c]);
     }
+  }
+}
+
+// Update and stores for group q x V replicas per lane; acc = the row sums.
+// The per-spin constants are read once per group (two float4 each; the
+// arrays are zero-padded to a multiple of 16 spins).
+template <int V>
+__device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, int r,
+                                              float (&acc)[8][V], const float (&sold)[8][V],
+                                              const float (&z)[V][8]) {
+  const int n = a.n, i_base = 8 * q;
+  const int Rp = (int)a.Rp;
+  const float inv_t = a.inv_t, alpha = a.alpha, oma = a.oma;
+  float* __restrict__ sn = a.s_new + r;
+  const float4* iv4 = reinterpret_cast<const float4*>(a.invn + i_base);
+  const float4* hv4 = reinterpret_cast<const float4*>(a.hn + i_base);
+  const float4 iv0 = __ldg(iv4), iv1 = __ldg(iv4 + 1), hv0 = __ldg(hv4), hv1 = __ldg(hv4 + 1);
+  const float invn[8] = {iv0.x, iv0.y, iv0.z, iv0.w, iv1.x, iv1.y, iv1.z, iv1.w};
+  const float hn[8] = {hv0.x, hv0.y, hv0.z, hv0.w, hv1.x, hv1.y, hv1.z, hv1.w};
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const int rc = r + c;
+    const bool valid = rc < a.R;
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq)
-      acc[qq][c] = nmfa_update(acc[qq][c], __ldg(a.invn + min(i_base + qq, n - 1)),
-                               __ldg(a.hn + min(i_base + qq, n - 1)), z[qq], inv_t, alpha, oma,
+      acc[qq][c] = nmfa_update(acc[qq][c], invn[qq], hn[qq], z[c][qq], inv_t, alpha, oma,
                                sold[qq][c]);
     const bool extra = valid && (a.s_hist != nullptr || a.last);
     if (extra) {
@@ -100,6 +119,14 @@ __device__ __forceinline__ void sparse_finish(const SparseStepArgs& a, int q, in
     else
       sn[i * Rp] = acc[qq][0];
   }
+}
+
+template <int V>
+__device__ __forceinline__ void sparse_finish(const SparseStepArgs& a, int q, int r,
+                                              float (&acc)[8][V], const float (&sold)[8][V]) {
+  float z[V][8];
+  sparse_noise<V>(a, q, r, z);
+  sparse_update<V>(a, q, r, acc, sold, z);
 }
 
 // V replicas per lane (1 or 2): with V = 2 every state access is one float2,
@@ -290,6 +317,8 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
     for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
       for (int u = 0; u < K; ++u) ld(__shfl_sync(0xffffffffu, off_l, qq * K + u), v[qq][u]);
+    float z[V][8];
+    sparse_noise<V>(a, q, r, z);  // independent of the loads above: overlaps their latency
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       float s2[V];
@@ -304,7 +333,7 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
-    sparse_finish<V>(a, q, r, acc, sold);
+    sparse_update<V>(a, q, r, acc, sold, z);
   }
 }
 
