@@ -46,6 +46,25 @@ struct SparseStepArgs {
   int last;
 };
 
+// p + off elements in ONE instruction (IMAD.WIDE.U32).  Written as plain C++
+// the compiler re-associates (s_old + r) + off into 64-bit sign-extended
+// arithmetic, four instructions per gather (profiles/r01/ell_notes.log).
+// Element offsets are < 2^31 (n x Rp bound checked at launch).  The result is
+// a generic pointer: accesses through it use __ldg / st.global (global space).
+template <typename T>
+__device__ __forceinline__ T* elem_addr(T* p, int off) {
+  uint64_t a;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(a) : "r"((uint32_t)off), "l"(reinterpret_cast<uint64_t>(p)));
+  return reinterpret_cast<T*>(a);
+}
+
+__device__ __forceinline__ void st_global(float* p, float x) {
+  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(x) : "memory");
+}
+__device__ __forceinline__ void st_global_v2(float* p, float x, float y) {
+  asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(x), "f"(y) : "memory");
+}
+
 // The N(0, sigma^2) noise of one warp's 8 spins (group q) x V replicas per
 // lane: injected (`a.noise`) or in-kernel Philox.  Independent of the state,
 // so the ELL kernel computes it while the group's gathers are in flight.
@@ -115,9 +134,9 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
     const int i = i_base + qq;
     if (i >= n) break;
     if constexpr (V == 2)
-      *reinterpret_cast<float2*>(sn + i * Rp) = make_float2(acc[qq][0], acc[qq][1]);
+      st_global_v2(elem_addr(sn, i * Rp), acc[qq][0], acc[qq][1]);
     else
-      sn[i * Rp] = acc[qq][0];
+      st_global(elem_addr(sn, i * Rp), acc[qq][0]);
   }
 }
 
@@ -150,7 +169,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   const int* __restrict__ idx = a.idx;
   const float* __restrict__ wts = a.w;
   auto ld = [&](int off, float* out) {  // V consecutive replicas of one state row
-    const Vec x = *reinterpret_cast<const Vec*>(so + off);
+    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr(so, off)));  // global, read-only
     if constexpr (V == 2) {
       out[0] = x.x;
       out[1] = x.y;
@@ -280,7 +299,7 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
   const int r = (slice * 32 + lane) * V;
   const float* __restrict__ so = a.s_old + r;
   auto ld = [&](int off, float* out) {
-    const Vec x = *reinterpret_cast<const Vec*>(so + off);
+    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr(so, off)));  // global, read-only
     if constexpr (V == 2) {
       out[0] = x.x;
       out[1] = x.y;
