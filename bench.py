@@ -514,7 +514,8 @@ def run_ours(args):
         peak = peaks.get("hbm_gbs")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
-                "kernel": "sparse NMFA step (CSR gather, fused epilogue)",
+                "kernel": ("sparse NMFA step (ELL gather, %d slots per row, fused epilogue)" % info["ell_slots"]
+                           if info.get("ell_slots") else "sparse NMFA step (CSR gather, fused epilogue)"),
                 "algorithmic_per_launch": f"R*N*8 + nnz*8 + (N+1)*4 = {byts:.4g} B",
                 "avg_launch_us": per_launch_s * 1e6, "peak_source": f"{peak_src} HBM copy"}
 

@@ -36,7 +36,7 @@ extern "C" {
 /* Kernel path chosen for a problem (internal detail, reported for tests). */
 #define NMFA_PATH_SMALL 0  /* n <= 256: persistent tcgen05 kernel, J in SMEM */
 #define NMFA_PATH_DENSE 1  /* dense n > 256: tcgen05 GEMM step, J streamed */
-#define NMFA_PATH_SPARSE 2 /* sparse n > 256: CSR gather step */
+#define NMFA_PATH_SPARSE 2 /* sparse n > 256: ELL (max degree <= 4) or CSR gather step */
 
 typedef struct nmfa_problem nmfa_problem_t;
 typedef struct nmfa_plan nmfa_plan_t;
@@ -50,6 +50,9 @@ typedef struct {
   int32_t j_exact;     /* 1 if every coupler is exact in the fp16 operand */
   int32_t int_weights; /* 1 if all weights and fields are integers */
   double j_scale;      /* power-of-two scale applied to J on device */
+  int32_t ell_slots;   /* sparse path: ELL row length (3 or 4) when the max
+                          degree is <= 4, 0 when rows use the CSR kernel */
+  int32_t reserved;
 } nmfa_problem_info_t;
 
 /* Build an immutable device-resident problem from the canonical coupler

@@ -56,7 +56,8 @@ SIGNATURES = {
 
 class ProblemInfo(ctypes.Structure):
     _fields_ = [("n", _i64), ("n_edges", _i64), ("density", _f64), ("is_dense", _i32),
-                ("path", _i32), ("j_exact", _i32), ("int_weights", _i32), ("j_scale", _f64)]
+                ("path", _i32), ("j_exact", _i32), ("int_weights", _i32), ("j_scale", _f64),
+                ("ell_slots", _i32), ("reserved", _i32)]
 
 
 _lib = None

@@ -140,14 +140,6 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
   }
 }
 
-template <int V>
-__device__ __forceinline__ void sparse_finish(const SparseStepArgs& a, int q, int r,
-                                              float (&acc)[8][V], const float (&sold)[8][V]) {
-  float z[V][8];
-  sparse_noise<V>(a, q, r, z);
-  sparse_update<V>(a, q, r, acc, sold, z);
-}
-
 // V replicas per lane (1 or 2): with V = 2 every state access is one float2,
 // halving the per-update address arithmetic and the uniform CSR overhead of
 // the V = 1 layout (the CSR path is issue-bound; profiles/r01/korder_ab.log).
@@ -202,6 +194,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   }
   float v[8][kFast][V];
   float acc[8][V];
+  float z[V][8];
   const int K0 = k0[0], seg = k0[7] + deg[7] - K0;  // the group's CSR entries [K0, K0 + seg)
   bool fast = seg <= 32;
 #pragma unroll
@@ -223,6 +216,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
           for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
         }
       }
+    sparse_noise<V>(a, q, r, z);  // overlaps the gathers' latency
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       float s2[V];
@@ -250,6 +244,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
           for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
         }
       }
+    sparse_noise<V>(a, q, r, z);
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       float s2[V];
@@ -273,7 +268,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
   }
-  sparse_finish<V>(a, q, r, acc, sold);
+  sparse_update<V>(a, q, r, acc, sold, z);
 }
 
 // ELL step for graphs of max degree <= K (K = 3: cubic, Moebius ladder; 4:

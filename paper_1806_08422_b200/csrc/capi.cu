@@ -35,12 +35,16 @@ static int upload(T** dst, const T* src, size_t count) {
 }
 
 // Path choice is internal (the reference picks dense vs CSR by density alone,
-// problem.py:97-99).  Measured on B200 at n = 2000: the tcgen05 path costs
-// ~N^2 R / 1.1e15 s per sweep, the CSR gather ~nnz R / 2.7e12 s, so the
-// tensor cores win down to ~0.2% density; the fp16 J image is capped at 1 GiB.
-static bool prefer_dense(int64_t n, int64_t n_edges) {
-  const double dense_cost = (double)n * (double)n / 1.1e15;
-  const double sparse_cost = 2.0 * (double)n_edges / 2.7e12;
+// problem.py:97-99).  Measured on B200, R = 1024 (profiles/r01/path_crossover.log):
+// * graphs of max degree <= 4 (ELL kernel) beat the tensor-core path at every
+//   n >= 512 (1.4x at n = 512, 6.5x at n = 16384);
+// * otherwise the tcgen05 path costs ~n^2 R / 5e14 s per sweep and the CSR
+//   gather ~nnz R / 5e11 s, so dense wins while n^2 < 1000 nnz (er_d10:
+//   dense at n = 8192, CSR at n = 16384); the fp16 J image is capped at 1 GiB.
+static bool prefer_dense(int64_t n, int64_t n_edges, int32_t ell_k) {
+  if (ell_k > 0) return false;
+  const double dense_cost = (double)n * (double)n / 5e14;
+  const double sparse_cost = 2.0 * (double)n_edges / 5e11;
   return (double)n * (double)n * 2.0 <= 1073741824.0 && dense_cost < sparse_cost;
 }
 
@@ -299,7 +303,7 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
       }
       if ((err = upload(&p->d_j_small, img.data(), img.size()))) break;
       p->path = NMFA_PATH_SMALL;
-    } else if (prefer_dense(n, n_edges)) {
+    } else if (prefer_dense(n, n_edges, p->ell_k)) {
       std::vector<float> jd((size_t)n * n, 0.f);
       for (int64_t k = 0; k < n_edges; ++k) {
         float v = (float)(w[k] / scale);
@@ -467,6 +471,8 @@ int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
   info->j_exact = p->j_exact;
   info->int_weights = p->int_weights;
   info->j_scale = p->j_scale;
+  info->ell_slots = p->ell_k;
+  info->reserved = 0;
   return NMFA_OK;
   NMFA_API_END
 }

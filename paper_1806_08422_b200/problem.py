@@ -198,7 +198,7 @@ class _DeviceProblem:
         return {"n": info.n, "n_edges": info.n_edges, "density": info.density,
                 "is_dense": bool(info.is_dense), "path": _native.PATH_NAMES[info.path],
                 "j_exact": bool(info.j_exact), "int_weights": bool(info.int_weights),
-                "j_scale": info.j_scale}
+                "j_scale": info.j_scale, "ell_slots": info.ell_slots}
 
     def set_path(self, path):
         code = {v: k for k, v in _native.PATH_NAMES.items()}[path]
