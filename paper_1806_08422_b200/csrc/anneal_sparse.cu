@@ -307,17 +307,8 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
   if (q_begin >= n_groups) return;
   const int q_end = min(q_begin + a.groups_per_warp, n_groups);
   const bool slot = lane < 8 * K;
-  int nx_idx = slot ? __ldg(a.ell_idx + q_begin * 8 * K + lane) : 0;
-  float nx_w = slot ? __ldg(a.ell_w + q_begin * 8 * K + lane) : 0.f;
-  for (int q = q_begin; q < q_end; ++q) {
-    const int off_l = nx_idx * Rp;
-    const float w_l = nx_w;
-    if (q + 1 < q_end && slot) {
-      nx_idx = __ldg(a.ell_idx + (q + 1) * 8 * K + lane);
-      nx_w = __ldg(a.ell_w + (q + 1) * 8 * K + lane);
-    }
+  auto issue = [&](int q, int off_l, float (&sold)[8][V], float (&v)[8][K][V]) {
     const int i_base = 8 * q;
-    float sold[8][V], v[8][K][V], acc[8][V];
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       if (i_base + qq < n) {
@@ -331,8 +322,8 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
     for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
       for (int u = 0; u < K; ++u) ld(__shfl_sync(0xffffffffu, off_l, qq * K + u), v[qq][u]);
-    float z[V][8];
-    sparse_noise<V>(a, q, r, z);  // independent of the loads above: overlaps their latency
+  };
+  auto sums = [&](float w_l, const float (&v)[8][K][V], float (&acc)[8][V]) {
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       float s2[V];
@@ -347,6 +338,21 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
+  };
+  int nx_idx = slot ? __ldg(a.ell_idx + q_begin * 8 * K + lane) : 0;
+  float nx_w = slot ? __ldg(a.ell_w + q_begin * 8 * K + lane) : 0.f;
+  for (int q = q_begin; q < q_end; ++q) {
+    const int off_l = nx_idx * Rp;
+    const float w_l = nx_w;
+    if (q + 1 < q_end && slot) {
+      nx_idx = __ldg(a.ell_idx + (q + 1) * 8 * K + lane);
+      nx_w = __ldg(a.ell_w + (q + 1) * 8 * K + lane);
+    }
+    float sold[8][V], v[8][K][V], acc[8][V];
+    issue(q, off_l, sold, v);
+    float z[V][8];
+    sparse_noise<V>(a, q, r, z);  // independent of the loads above: overlaps their latency
+    sums(w_l, v, acc);
     sparse_update<V>(a, q, r, acc, sold, z);
   }
 }
