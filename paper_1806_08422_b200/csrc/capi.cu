@@ -215,6 +215,7 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
   for (int64_t i = 0; i < n; ++i)
     if (h[i] != std::floor(h[i])) ints = false;
   p->int_weights = ints;
+  for (int64_t i = 0; i < n && !p->has_field; ++i) p->has_field = h[i] != 0.0;
   double scale = 1.0;
   if (wmax > 0.0) {
     bool exact1 = wmax <= 2048.0;

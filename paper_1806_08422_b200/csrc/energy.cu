@@ -8,6 +8,7 @@
 // over edge chunks are float64 and reduced in a fixed order (deterministic);
 // for integer weights every partial is an exact integer, so the result is
 // bit-identical to the reference's float64 dot for any summation order.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -34,21 +35,23 @@ __global__ void pack_bits_kernel(const int8_t* __restrict__ cfg, long long R, in
   }
 }
 
-// part[c][r]: chunk c of the canonical edge list (c < chunks), and the field
-// term in row `chunks`.
+// part[c][r]: rows c < e_chunks are chunks of the canonical edge list, rows
+// e_chunks <= c < e_chunks + f_chunks chunks of the spins for the field term
+// (no field rows when h = 0).  Each row is one grid row of warps, 32 replicas
+// per warp.
 __global__ void __launch_bounds__(128) energy_partial_kernel(
     const uint32_t* __restrict__ bits, long long R, long long W, int n, long long n_edges,
     const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
-    const double* __restrict__ ew, const double* __restrict__ h, long long chunks,
-    double* __restrict__ part) {
+    const double* __restrict__ ew, const double* __restrict__ h, long long e_chunks,
+    long long f_chunks, double* __restrict__ part) {
   const int lane = threadIdx.x & 31;
   const long long wd = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (wd >= W) return;
   const long long r = wd * 32 + lane;
   const long long c = blockIdx.y;
   double acc = 0.0;
-  if (c < chunks) {
-    const long long k0 = n_edges * c / chunks, k1 = n_edges * (c + 1) / chunks;
+  if (c < e_chunks) {
+    const long long k0 = n_edges * c / e_chunks, k1 = n_edges * (c + 1) / e_chunks;
     for (long long k = k0; k < k1; ++k) {
       const uint32_t x = __ldg(bits + (long long)__ldg(ei + k) * W + wd) ^
                          __ldg(bits + (long long)__ldg(ej + k) * W + wd);
@@ -56,7 +59,9 @@ __global__ void __launch_bounds__(128) energy_partial_kernel(
       acc += ((x >> lane) & 1u) ? -w : w;
     }
   } else {
-    for (int i = 0; i < n; ++i) {
+    const long long f = c - e_chunks;
+    const int i0 = (int)(n * f / f_chunks), i1 = (int)(n * (f + 1) / f_chunks);
+    for (int i = i0; i < i1; ++i) {
       const double hv = __ldg(h + i);
       const uint32_t b = __ldg(bits + (long long)i * W + wd);
       acc += ((b >> lane) & 1u) ? -hv : hv;
@@ -66,15 +71,20 @@ __global__ void __launch_bounds__(128) energy_partial_kernel(
 }
 
 __global__ void energy_reduce_kernel(const double* __restrict__ part, long long R,
-                                     long long chunks, double* __restrict__ e) {
+                                     long long e_chunks, long long f_chunks,
+                                     double* __restrict__ e) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
-  double pair = 0.0;
-  for (long long c = 0; c < chunks; ++c) pair += part[c * R + r];
-  e[r] = pair + part[chunks * R + r];  // pair + field, like problem.py:153-154
+  double pair = 0.0, field = 0.0;
+  for (long long c = 0; c < e_chunks; ++c) pair += part[c * R + r];
+  for (long long c = e_chunks; c < e_chunks + f_chunks; ++c) field += part[c * R + r];
+  e[r] = pair + field;  // pair + field, like problem.py:153-154
 }
 
-int64_t energy_chunks_for(const nmfa_problem* p, int64_t n_cfg) {
+// Edge chunks: enough warps for ~8 per SM, >= 512 edges each.  Field chunks:
+// 2048 spins each (a single serial row cost 14 ms at n = 131072), none when
+// h = 0 (the field term is then +0.0 exactly, as before).
+static int64_t edge_chunks_for(const nmfa_problem* p, int64_t n_cfg) {
   const int64_t W = (n_cfg + 31) / 32;
   const int64_t nblk = (W + 3) / 4;
   int64_t want = (148 * 8 + nblk - 1) / nblk;
@@ -85,18 +95,34 @@ int64_t energy_chunks_for(const nmfa_problem* p, int64_t n_cfg) {
   return want;
 }
 
+static int64_t field_chunks_for(const nmfa_problem* p) {
+  return p->has_field ? std::max<int64_t>(1, (p->n + 2047) / 2048) : 0;
+}
+
+// Scratch rows minus one (callers allocate (chunks + 1) * n_cfg doubles).
+int64_t energy_chunks_for(const nmfa_problem* p, int64_t n_cfg) {
+  return edge_chunks_for(p, n_cfg) + field_chunks_for(p) - 1;
+}
+
 int launch_energy(const nmfa_problem* p, const int8_t* cfg, int64_t R, double* energy,
                   uint32_t* bits, double* part, int64_t chunks, cudaStream_t st) {
   const long long W = (R + 31) / 32;
   dim3 g1((unsigned)((p->n + 127) / 128), (unsigned)W);
   pack_bits_kernel<<<g1, 256, 0, st>>>(cfg, R, (int)p->n, W, bits);
   NMFA_LAUNCH_CHECK();
-  // `part` holds chunks+1 rows; the allocation sites size it (chunks+1)*R.
-  dim3 g2((unsigned)((W + 3) / 4), (unsigned)(chunks + 1));
+  // `part` holds chunks + 1 rows (energy_chunks_for): field rows first claimed
+  const long long f_chunks = field_chunks_for(p);
+  const long long e_chunks = chunks + 1 - f_chunks;
+  if (e_chunks < 1) {
+    set_error("energy scratch too small");
+    return NMFA_ERR_ARG;
+  }
+  dim3 g2((unsigned)((W + 3) / 4), (unsigned)(e_chunks + f_chunks));
   energy_partial_kernel<<<g2, 128, 0, st>>>(bits, R, W, (int)p->n, p->n_edges, p->d_e_i,
-                                            p->d_e_j, p->d_e_w, p->d_h, chunks, part);
+                                            p->d_e_j, p->d_e_w, p->d_h, e_chunks, f_chunks, part);
   NMFA_LAUNCH_CHECK();
-  energy_reduce_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(part, R, chunks, energy);
+  energy_reduce_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(part, R, e_chunks, f_chunks,
+                                                                   energy);
   NMFA_LAUNCH_CHECK();
   add_launches(3);
   return NMFA_OK;

@@ -40,6 +40,7 @@ struct nmfa_problem {
   int32_t path = NMFA_PATH_SPARSE;
   bool j_exact = true;
   bool int_weights = true;
+  bool has_field = false;  // some h_i != 0 (the energy's field term is skipped otherwise)
   double j_scale = 1.0;    // J_dev = J / j_scale (power of two); inv_norm carries j_scale
   double max_row_abs = 0.0; // max_i sum_j |J_ij| (exactness bound of tensor-core energies)
   int32_t np = 0;          // n padded to a multiple of 16 (tensor-core paths)
