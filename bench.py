@@ -38,9 +38,9 @@ WORKLOADS = {
                    "Moebius ladder n=100, 37888 reads/GPU, t_f=1000"),
     "g2000": ("gen_dense_maxcut(2000, 0.01, 7)", 2000, 4096, 1000,
               "G-set-style gen_dense_maxcut(2000,0.01,7), 4096 reads/GPU, t_f=1000"),
-    # the CSR path where it is the routed one (large, low-degree sparse instance)
+    # the sparse path where it is the routed one (large, low-degree instance: ELL kernel)
     "moebius131072": ("moebius_ladder(131072)", 131072, 1024, 200,
-                      "Moebius ladder n=131072 (CSR path), 1024 reads/GPU, t_f=200"),
+                      "Moebius ladder n=131072 (sparse ELL path), 1024 reads/GPU, t_f=200"),
     # exhaustive ground state (brute_force_ground) at the reference's limit
     "ground26": ("gen_sk(26, 1)", 26, 1, 1, "exact ground state of gen_sk(26,1) by Gray-code enumeration"),
     # config 5: J generated on device, row-sharded over the ranks (strong scaling)
