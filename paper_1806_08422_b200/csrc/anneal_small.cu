@@ -49,8 +49,12 @@ struct SmallArgs {
 constexpr uint32_t kRowsPerCta = 128;
 constexpr uint32_t kLboA = (kRowsPerCta / 8) * 128;  // A: K core matrices 2048 B apart
 
+#ifndef NMFA_SMALL_MINB
+#define NMFA_SMALL_MINB 1  // blocks per SM the register budget targets (A/B knob)
+#endif
+
 template <bool kInjected>
-__global__ void __launch_bounds__(512, 1) small_anneal_kernel(const SmallArgs a) {
+__global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(const SmallArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int np = a.np;
   uint8_t* sJ = smem;
