@@ -75,3 +75,22 @@ def test_backend_matches_reference_operator_signatures():
     for name in ("anneal_dense", "anneal_sparse", "gray_ground"):
         assert list(inspect.signature(getattr(b200, name)).parameters) == \
             list(inspect.signature(getattr(refk, name)).parameters), name
+
+
+def test_problem_info_struct_matches_header(tmp_path):
+    """The ctypes mirror of nmfa_problem_info_t has the C layout (size and every
+    field offset, compiled from the header with gcc)."""
+    import ctypes
+    fields = [f for f, _ in _native.ProblemInfo._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"nmfa_b200.h\"\nint main(void){\n"
+                   "printf(\"%zu\\n\", sizeof(nmfa_problem_info_t));\n" +
+                   "".join(f"printf(\"%zu\\n\", offsetof(nmfa_problem_info_t, {f}));\n" for f in fields) +
+                   "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [ctypes.sizeof(_native.ProblemInfo)] + [getattr(_native.ProblemInfo, f).offset
+                                                   for f in fields]
+    assert got == want, (got, want)

@@ -57,6 +57,16 @@ def mixed(n, seed, h=False):
     return nb.IsingProblem.from_arrays(n, e[:, 0], e[:, 1], rng.normal(size=len(e)), hv)
 
 
+def random_degree(n, d, seed):
+    """About n*d/2 distinct random couplers (mean degree ~d), +1 weights."""
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, n, n * d // 2)
+    b = rng.integers(0, n, n * d // 2)
+    keep = a != b
+    key = np.unique(np.minimum(a, b)[keep] * n + np.maximum(a, b)[keep])
+    return nb.IsingProblem.from_arrays(n, key // n, key % n, np.ones(key.size))
+
+
 GRAPHS = {
     "moebius_1000": lambda: nb.moebius_ladder(1000),
     "cubic_302": lambda: nb.gen_cubic_maxcut(302, 4),
@@ -125,3 +135,19 @@ def test_ell_torus_matches_oracle():
     assert np.abs(S - ref).max() <= 2e-2
     firm = np.abs(ref) > 2e-2
     assert np.array_equal(np.sign(S[firm]), np.sign(ref[firm]))
+
+
+@pytest.mark.parametrize("make,path,slots", [
+    (lambda: nb.gen_cubic_maxcut(512, 1), "sparse", 3),
+    (lambda: nb.moebius_ladder(1000), "sparse", 3),
+    (lambda: torus(23, 23), "sparse", 4),
+    (lambda: mixed(301, 7), "sparse", 3),
+    (lambda: nb.gen_dense_maxcut(2000, 0.01, 7), "dense", 0),     # G2000 stand-in (C4)
+    (lambda: random_degree(16384, 10, 1), "sparse", 0),  # n^2 > 1000 nnz: CSR
+    (lambda: random_degree(8192, 10, 1), "dense", 0),
+])
+def test_path_router(make, path, slots):
+    """capi.cu prefer_dense, refit from profiles/r01/path_crossover.log: max degree
+    <= 4 always takes the ELL kernel; otherwise dense while n^2 < 1000 nnz."""
+    info = make().device_info()
+    assert info["path"] == path and info["ell_slots"] == slots, info
