@@ -30,6 +30,7 @@ struct SparseStepArgs {
   const int32_t* ell_idx;  // ELL rows (problem ell_k > 0), else null
   const float* ell_w;
   int groups_per_warp;     // ELL kernel: consecutive spin groups per warp
+  uint32_t elem_bytes;     // sizeof(float), passed at run time (see elem_addr)
   int slices_per_block;    // ELL kernel: replica slices per block (1, 2, 4, 8)
   const float* invn;
   const float* hn;
@@ -51,10 +52,22 @@ struct SparseStepArgs {
 // arithmetic, four instructions per gather (profiles/r01/ell_notes.log).
 // Element offsets are < 2^31 (n x Rp bound checked at launch).  The result is
 // a generic pointer: accesses through it use __ldg / st.global (global space).
-template <typename T>
-__device__ __forceinline__ T* elem_addr(T* p, int off) {
+// kImad: the multiplier is a kernel argument (4), so the address is one
+// IMAD.WIDE.U32; otherwise the immediate 4 gives a LEA / LEA.HI.X pair on the
+// ALU pipe.  The ELL kernel's FMA-pipe-heavy mix prefers the LEA pair (4.19e11
+// vs 4.0e11 spin-updates/s), the CSR kernel the IMAD (2.75e11 vs 2.49e11)
+// (profiles/r01/ell_notes.log).
+template <bool kImad, typename T>
+__device__ __forceinline__ T* elem_addr(T* p, int off, uint32_t elem_bytes) {
   uint64_t a;
-  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(a) : "r"((uint32_t)off), "l"(reinterpret_cast<uint64_t>(p)));
+  if constexpr (kImad)
+    asm("mad.wide.u32 %0, %1, %2, %3;"
+        : "=l"(a)
+        : "r"((uint32_t)off), "r"(elem_bytes), "l"(reinterpret_cast<uint64_t>(p)));
+  else
+    asm("mad.wide.u32 %0, %1, 4, %2;"
+        : "=l"(a)
+        : "r"((uint32_t)off), "l"(reinterpret_cast<uint64_t>(p)));
   return reinterpret_cast<T*>(a);
 }
 
@@ -93,7 +106,7 @@ __device__ __forceinline__ void sparse_noise(const SparseStepArgs& a, int q, int
 // Update and stores for group q x V replicas per lane; acc = the row sums.
 // The per-spin constants are read once per group (two float4 each; the
 // arrays are zero-padded to a multiple of 16 spins).
-template <int V>
+template <int V, bool kImad>
 __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, int r,
                                               float (&acc)[8][V], const float (&sold)[8][V],
                                               const float (&z)[V][8]) {
@@ -134,9 +147,9 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
     const int i = i_base + qq;
     if (i >= n) break;
     if constexpr (V == 2)
-      st_global_v2(elem_addr(sn, i * Rp), acc[qq][0], acc[qq][1]);
+      st_global_v2(elem_addr<kImad>(sn, i * Rp, a.elem_bytes), acc[qq][0], acc[qq][1]);
     else
-      st_global(elem_addr(sn, i * Rp), acc[qq][0]);
+      st_global(elem_addr<kImad>(sn, i * Rp, a.elem_bytes), acc[qq][0]);
   }
 }
 
@@ -161,7 +174,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   const int* __restrict__ idx = a.idx;
   const float* __restrict__ wts = a.w;
   auto ld = [&](int off, float* out) {  // V consecutive replicas of one state row
-    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr(so, off)));  // global, read-only
+    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr<true>(so, off, a.elem_bytes)));  // global, read-only
     if constexpr (V == 2) {
       out[0] = x.x;
       out[1] = x.y;
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
   }
-  sparse_update<V>(a, q, r, acc, sold, z);
+  sparse_update<V, true>(a, q, r, acc, sold, z);
 }
 
 // ELL step for graphs of max degree <= K (K = 3: cubic, Moebius ladder; 4:
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
   const int r = (slice * 32 + lane) * V;
   const float* __restrict__ so = a.s_old + r;
   auto ld = [&](int off, float* out) {
-    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr(so, off)));  // global, read-only
+    const Vec x = __ldg(reinterpret_cast<const Vec*>(elem_addr<false>(so, off, a.elem_bytes)));  // global, read-only
     if constexpr (V == 2) {
       out[0] = x.x;
       out[1] = x.y;
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const Sp
     float z[V][8];
     sparse_noise<V>(a, q, r, z);  // independent of the loads above: overlaps their latency
     sums(w_l, v, acc);
-    sparse_update<V>(a, q, r, acc, sold, z);
+    sparse_update<V, false>(a, q, r, acc, sold, z);
   }
 }
 
@@ -396,6 +409,7 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   a.oma = pl->oma;
   a.sigma = pl->sigma;
   a.key_base = key_base;
+  a.elem_bytes = (uint32_t)sizeof(float);
   a.noise = noise;
   a.cfg = cfg;
   a.s_out = s_out;
