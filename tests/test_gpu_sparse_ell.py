@@ -151,3 +151,23 @@ def test_path_router(make, path, slots):
     <= 4 always takes the ELL kernel; otherwise dense while n^2 < 1000 nnz."""
     info = make().device_info()
     assert info["path"] == path and info["ell_slots"] == slots, info
+
+
+@pytest.mark.parametrize("integer_h", [True, False])
+def test_energy_field_term_in_chunks(integer_h):
+    """n = 5000 > 2048: the field term h.c runs as three spin chunks
+    (energy.cu). Integer fields stay bit-exact; real fields within 1e-12."""
+    n = 5000
+    rng = np.random.default_rng(3)
+    base = nb.gen_cubic_maxcut(n, 2)
+    h = rng.integers(-3, 4, n).astype(np.float64) if integer_h else rng.normal(size=n)
+    p = nb.IsingProblem.from_arrays(n, base.edges_i, base.edges_j, base.edge_weights, h)
+    res = nb.sample(p, nb.NmfaParams(t_f=30, seed=4), 96)
+    cfg = res.configs.cpu().numpy().astype(np.float64)
+    op = O.problem_from_edges(n, p.edges_i, p.edges_j, p.edge_weights, h)
+    want = O.energies(op, cfg)
+    got = res.energies.cpu().numpy()
+    if integer_h:
+        assert np.array_equal(got, want)
+    else:
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-9)
