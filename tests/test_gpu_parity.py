@@ -281,6 +281,13 @@ def test_g2000_energy_distribution(G, path):
     print(f"g2000[{path}] mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
           f"min_ref={ref.min()} se={se:.2f}")
     assert abs(e.mean() - ref.mean()) < 4 * se
+    # SURVEY 8(d) C4 success criterion: E <= E*, the reference's 10th-percentile energy
+    e_star = np.quantile(ref, 0.1)
+    p_ref, p_gpu = np.mean(ref <= e_star), np.mean(e <= e_star)
+    pool = (p_ref * ref.size + p_gpu * e.size) / (ref.size + e.size)
+    z = (p_gpu - p_ref) / np.sqrt(pool * (1 - pool) * (1 / ref.size + 1 / e.size))
+    print(f"g2000[{path}] E*={e_star} p_ref={p_ref:.3f} p_gpu={p_gpu:.3f} z={z:.2f}")
+    assert abs(z) < 3.5
 
 
 def test_host_entry_point_matches_device_api():
