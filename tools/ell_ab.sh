@@ -1,9 +1,8 @@
-# unit-weight ELL A/B (NMFA_ELL_UNIT=0 keeps the weighted kernel) + identity tests
+# toroidal (degree 4) graphs: ELL K=4 (V=2 / V=1) vs CSR
 mkdir -p gpurun_out
 python -m paper_1806_08422_b200.build > /dev/null 2>&1
-timeout 600 python -m pytest tests/test_gpu_sparse_ell.py -m gpu -x -q 2>&1 | tail -1
 P="timeout 200 python tools/prof_sparse_large.py"
-for rep in 1 2; do
-  echo "-- ELL weighted"; NMFA_ELL_UNIT=0 $P 131072 1024
-  echo "-- ELL unit"; $P 131072 1024
-done
+echo "-- torus ELL V=2"; PROF_TORUS=1 $P 131044 1024
+echo "-- torus ELL V=1"; PROF_TORUS=1 NMFA_SPARSE_V=1 $P 131044 1024
+echo "-- torus CSR"; PROF_TORUS=1 NMFA_SPARSE_CSR=1 $P 131044 1024
+echo "-- torus ELL G sweep"; for g in 2 4 8; do PROF_TORUS=1 NMFA_ELL_G=$g $P 131044 1024; done

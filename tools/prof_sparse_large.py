@@ -7,7 +7,19 @@ import paper_1806_08422_b200 as nb
 
 peaks = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))
 hbm = next(v for k, v in peaks.items() if "hbm" in k.lower() and isinstance(v, (int, float)))
+def torus(n):
+    import numpy as np
+    c = int(round(n ** 0.5))
+    v = np.arange(c * c).reshape(c, c)
+    a = np.concatenate([v.ravel(), v.ravel()])
+    b = np.concatenate([np.roll(v, -1, 1).ravel(), np.roll(v, -1, 0).ravel()])
+    w = np.where(np.random.default_rng(c).random(a.size) < 0.5, 1.0, -1.0)
+    return nb.IsingProblem.from_arrays(c * c, np.minimum(a, b), np.maximum(a, b), w)
+
+
 cases = [("moebius", lambda n: nb.moebius_ladder(n)), ("cubic", lambda n: nb.gen_cubic_maxcut(n, 1))]
+if os.environ.get("PROF_TORUS"):
+    cases = [("torus", torus)]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 t_f = 100
@@ -27,5 +39,5 @@ for name, mk in cases:
     nnz = 2 * p.num_edges
     byts = R * n * 8 + nnz * 8 + (n + 1) * 4
     gbs = byts / (us * 1e-6) / 1e9
-    print(f"{name} n={n} R={R} path={info['path']}: {us:.1f} us/step  {n*R/(us*1e-6):.3g} su/s  "
+    print(f"{name} n={p.n} R={R} path={info['path']}: {us:.1f} us/step  {n*R/(us*1e-6):.3g} su/s  "
           f"{gbs:.0f} GB/s algorithmic = {gbs/hbm:.2f} of HBM {hbm:.0f}", flush=True)
