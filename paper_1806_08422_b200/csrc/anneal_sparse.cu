@@ -270,15 +270,28 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
 #pragma unroll
           for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);
         }
-      for (int k = k0[qq] + kFast; k < k0[qq] + deg[qq]; ++k) {  // rows longer than kFast
-        float x[V];
-        ld(__ldg(idx + k) * Rp, x);
-        const float wv = __ldg(wts + k);
-#pragma unroll
-        for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, x[c], s2[c]);
-      }
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
+    }
+    // entries beyond kFast: round u gathers entry u of all 8 rows at once (8
+    // loads in flight instead of one), then adds them in each row's CSR order
+    int dmax = 0;
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) dmax = max(dmax, deg[qq]);
+    for (int u = kFast; u < dmax; ++u) {
+      float x[8][V], wv[8];
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        if (u < deg[qq]) {
+          ld(__ldg(idx + k0[qq] + u) * Rp, x[qq]);
+          wv[qq] = __ldg(wts + k0[qq] + u);
+        }
+      }
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq)
+        if (u < deg[qq])
+#pragma unroll
+          for (int c = 0; c < V; ++c) acc[qq][c] = fmaf(wv[qq], x[qq][c], acc[qq][c]);
     }
   }
   sparse_update<V, true>(a, q, r, acc, sold, z);

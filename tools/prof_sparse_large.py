@@ -18,8 +18,20 @@ def torus(n):
 
 
 cases = [("moebius", lambda n: nb.moebius_ladder(n)), ("cubic", lambda n: nb.gen_cubic_maxcut(n, 1))]
+def er(n, d, seed=1):
+    """about n*d/2 random couplers (Poisson degrees, mean d), +1 weights"""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    a, b = rng.integers(0, n, n * d // 2), rng.integers(0, n, n * d // 2)
+    keep = a != b
+    key = np.unique(np.minimum(a, b)[keep] * n + np.maximum(a, b)[keep])
+    return nb.IsingProblem.from_arrays(n, key // n, key % n, np.ones(key.size))
+
+
 if os.environ.get("PROF_TORUS"):
     cases = [("torus", torus)]
+if os.environ.get("PROF_ER"):
+    cases = [(f"er_d{d}", (lambda d: lambda n: er(n, d))(d)) for d in map(int, os.environ["PROF_ER"].split(","))]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 t_f = 100
