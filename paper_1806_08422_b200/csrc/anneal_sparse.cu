@@ -14,6 +14,9 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef NMFA_CSR_ROUNDS
+#define NMFA_CSR_ROUNDS 2
+#endif
 #ifndef NMFA_ELL_MINB
 #define NMFA_ELL_MINB 2  // ELL kernel blocks per SM (128 registers, no spill at V = 2)
 #endif
@@ -187,6 +190,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   // cooperative load; then every gather of the 8 spins is issued before the
   // first use (degree <= kFast unrolled, longer rows in a general loop).
   constexpr int kFast = 3;  // unrolled row length (cubic / Moebius ladder); longer rows loop
+  constexpr int kRounds = NMFA_CSR_ROUNDS;  // entries per row gathered per round beyond kFast
   const int i_base = 8 * q;
   const int pl = lane <= 8 ? __ldg(a.ptr + min(i_base + lane, n)) : 0;
   int k0[8], deg[8];
@@ -278,20 +282,24 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     int dmax = 0;
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) dmax = max(dmax, deg[qq]);
-    for (int u = kFast; u < dmax; ++u) {
-      float x[8][V], wv[8];
+    for (int u = kFast; u < dmax; u += kRounds) {
+      float x[kRounds][8][V], wv[kRounds][8];
 #pragma unroll
-      for (int qq = 0; qq < 8; ++qq) {
-        if (u < deg[qq]) {
-          ld(__ldg(idx + k0[qq] + u) * Rp, x[qq]);
-          wv[qq] = __ldg(wts + k0[qq] + u);
+      for (int j = 0; j < kRounds; ++j)
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          if (u + j < deg[qq]) {
+            ld(__ldg(idx + k0[qq] + u + j) * Rp, x[j][qq]);
+            wv[j][qq] = __ldg(wts + k0[qq] + u + j);
+          }
         }
-      }
 #pragma unroll
-      for (int qq = 0; qq < 8; ++qq)
-        if (u < deg[qq])
+      for (int j = 0; j < kRounds; ++j)
 #pragma unroll
-          for (int c = 0; c < V; ++c) acc[qq][c] = fmaf(wv[qq], x[qq][c], acc[qq][c]);
+        for (int qq = 0; qq < 8; ++qq)
+          if (u + j < deg[qq])
+#pragma unroll
+            for (int c = 0; c < V; ++c) acc[qq][c] = fmaf(wv[j][qq], x[j][qq][c], acc[qq][c]);
     }
   }
   sparse_update<V, true>(a, q, r, acc, sold, z);
