@@ -38,13 +38,14 @@ static int upload(T** dst, const T* src, size_t count) {
 // problem.py:97-99).  Measured on B200, R = 1024 (profiles/r01/path_crossover.log):
 // * graphs of max degree <= 4 (ELL kernel) beat the tensor-core path at every
 //   n >= 512 (1.4x at n = 512, 6.5x at n = 16384);
-// * otherwise the tcgen05 path costs ~n^2 R / 5e14 s per sweep and the CSR
-//   gather ~nnz R / 5e11 s, so dense wins while n^2 < 1000 nnz (er_d10:
-//   dense at n = 8192, CSR at n = 16384); the fp16 J image is capped at 1 GiB.
+// * otherwise the tcgen05 path costs ~n^2 R / 5.5e14 s per sweep and the CSR
+//   gather ~nnz R / 9e11 s, so dense wins while n^2 < 611 nnz (er_d10: dense
+//   at n = 4096, CSR from n = 8192; er_d20: CSR from n = 16384); the fp16 J
+//   image is capped at 1 GiB.
 static bool prefer_dense(int64_t n, int64_t n_edges, int32_t ell_k) {
   if (ell_k > 0) return false;
-  const double dense_cost = (double)n * (double)n / 5e14;
-  const double sparse_cost = 2.0 * (double)n_edges / 5e11;
+  const double dense_cost = (double)n * (double)n / 5.5e14;
+  const double sparse_cost = 2.0 * (double)n_edges / 9e11;
   return (double)n * (double)n * 2.0 <= 1073741824.0 && dense_cost < sparse_cost;
 }
 

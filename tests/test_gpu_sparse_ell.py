@@ -143,12 +143,14 @@ def test_ell_torus_matches_oracle():
     (lambda: torus(23, 23), "sparse", 4),
     (lambda: mixed(301, 7), "sparse", 3),
     (lambda: nb.gen_dense_maxcut(2000, 0.01, 7), "dense", 0),     # G2000 stand-in (C4)
-    (lambda: random_degree(16384, 10, 1), "sparse", 0),  # n^2 > 1000 nnz: CSR
-    (lambda: random_degree(8192, 10, 1), "dense", 0),
+    (lambda: random_degree(16384, 10, 1), "sparse", 0),  # n^2 > 611 nnz: CSR
+    (lambda: random_degree(8192, 10, 1), "sparse", 0),
+    (lambda: random_degree(8192, 20, 1), "dense", 0),
+    (lambda: random_degree(4096, 10, 1), "dense", 0),
 ])
 def test_path_router(make, path, slots):
     """capi.cu prefer_dense, refit from profiles/r01/path_crossover.log: max degree
-    <= 4 always takes the ELL kernel; otherwise dense while n^2 < 1000 nnz."""
+    <= 4 always takes the ELL kernel; otherwise dense while n^2 < 611 nnz."""
     info = make().device_info()
     assert info["path"] == path and info["ell_slots"] == slots, info
 
