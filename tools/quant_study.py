@@ -5,6 +5,7 @@ Same setup as tests/test_gpu_parity.py::test_dense_large_injected_noise_matches_
   f16       : s -> fp16(s)                          (today's operand)
   f16hilo   : fp16(s) + fp16(s - fp16(s))           (hi+lo both as operands)
   fixK      : s -> round(s * 2^K) / 2^K             (fixed point, K fractional bits)
+  tanh11    : exact operand, tanh rounded to ~11 bits (a tanh.approx.f32 stand-in)
 The sum itself is exact float64 here (the int32 accumulation is exact too)."""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
@@ -27,11 +28,16 @@ rng = np.random.Generator(np.random.Philox(key=99))
 noise = rng.standard_normal((R, t_f, n)) * 0.15
 
 
-def run(q):
+def tanh11(x):
+    """tanh with ~2^-11 relative error (float16 rounding), a stand-in for tanh.approx.f32"""
+    return np.tanh(x).astype(np.float16).astype(np.float64)
+
+
+def run(q, th=np.tanh):
     S = np.zeros((R, n))
     for t in range(t_f):
         phi = (q(S) @ J) / norm + noise[:, t, :]
-        S = alpha * (-np.tanh(phi / temps[t])) + (1 - alpha) * S
+        S = alpha * (-th(phi / temps[t])) + (1 - alpha) * S
     return S
 
 
@@ -41,8 +47,16 @@ modes = {"f16": lambda s: s.astype(np.float16).astype(np.float64),
              s.astype(np.float16).astype(np.float64))}
 for K in (11, 13, 14, 15, 16, 20):
     modes[f"fix{K}"] = (lambda K: lambda s: np.clip(np.round(s * 2.0 ** K), -2.0 ** K, 2.0 ** K - 1) / 2.0 ** K)(K)
+f16 = modes["f16"]
+modes["tanh11"] = None
+modes["f16+tanh11"] = None
 for name, q in modes.items():
-    S = run(q)
+    if name == "tanh11":
+        S = run(lambda s: s, tanh11)
+    elif name == "f16+tanh11":
+        S = run(f16, tanh11)
+    else:
+        S = run(q)
     err = np.abs(S - ref)
     flips = np.mean(np.sign(S) != np.sign(ref))
     print(f"n={n} {name:8s} mean|dS|={err.mean():.2e}  frac(|dS|>2e-2)={np.mean(err > 2e-2):.2e}  "
