@@ -1,11 +1,14 @@
-// Sparse NMFA step (CSR gather), one launch per step.
+// Sparse NMFA step, one launch per step: ELL gather (max degree <= 4) or
+// CSR gather (any degree).
 // State layout: S[i][r] fp32, replicas contiguous (Rp = R rounded up to 32),
 // ping-pong between two buffers (synchronous update, SPEC: all mean fields
-// from the incoming S).  One warp owns a group of 8 consecutive spins for 32
-// consecutive replicas: every CSR entry (j, w) is a warp-uniform broadcast
-// and the gather S[j][r..r+31] is one coalesced 128-byte load.  The group
-// matches the Philox counter granularity, so one Philox call per thread
-// feeds its eight spins (common.cuh noise identity).
+// from the incoming S).  One warp owns a group of 8 consecutive spins for
+// 32V consecutive replicas (V = 2: one float2 per lane): every row entry
+// (j, w) is a warp-uniform broadcast and the gather S[j][r..r+32V) is one
+// coalesced load.  The group matches the Philox counter granularity, so one
+// Philox call per replica feeds its eight spins (common.cuh noise identity).
+// Both kernels sum each row in CSR order from +0, so they agree bit for bit.
+// Measured design steps: profiles/r01/ell_notes.log, DESIGN.md section 6.
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
 #include <algorithm>
 #include <cstdlib>
