@@ -423,3 +423,29 @@ def gray_ground_fast(problem):
         _gray_jit = _walk
     return _gray_jit(problem.csr_indptr, problem.csr_indices, problem.csr_weights,
                      np.asarray(problem.h, dtype=np.float64))
+
+
+def device_normals(seed, replicas, t, n, sigma):
+    """The in-kernel noise spec (common.cuh normal8; DESIGN §2 "Noise stream"):
+    N(0, sigma^2) for global replicas `replicas`, 0-based step t, spins 0..n-1.
+    key = (lo32, hi32)(seed + r); counter = (i >> 3, t, 0x4E4D4641, 0); word
+    w = (i & 7) >> 1 is one Box-Muller pair: u1 = ((w >> 12) + 1/2) 2^-20,
+    angle = 2 pi (w & 0xFFF) / 4096, spin 8q + 2w -> r cos, 8q + 2w + 1 -> r sin.
+    float64 here; the device uses MUFU approximations (agree to ~1e-6)."""
+    replicas = np.asarray(replicas, dtype=np.int64)
+    q = np.arange((n + 7) // 8, dtype=np.uint32)
+    out = np.zeros((replicas.size, n))
+    for a, r in enumerate(replicas):
+        key = (int(seed) + int(r)) & 0xFFFFFFFFFFFFFFFF
+        words = philox4x32_10(q, np.uint32(t), np.uint32(0x4E4D4641), np.uint32(0),
+                              key & 0xFFFFFFFF, key >> 32)
+        z = np.zeros((q.size, 8))
+        for w in range(4):
+            x = words[w].astype(np.int64)
+            u1 = ((x >> 12) + 0.5) * 2.0 ** -20
+            rad = sigma * np.sqrt(-2.0 * np.log(u1))
+            ang = (x & 0xFFF) * (2.0 * np.pi / 4096.0)
+            z[:, 2 * w] = rad * np.cos(ang)
+            z[:, 2 * w + 1] = rad * np.sin(ang)
+        out[a] = z.reshape(-1)[:n]
+    return out

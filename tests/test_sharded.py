@@ -80,3 +80,15 @@ def test_exchange_slices_gathers_every_shard():
     for g in range(world):
         assert np.array_equal(out[g][: world * per * sb], want)
         assert np.all(out[g][world * per * sb:] == 255)   # bytes past the slabs untouched
+
+
+def test_device_normals_spec_moments():
+    """The oracle twin of the in-kernel noise (tests/test_gpu_noise.py pins the
+    kernels to it): N(0, sigma^2) moments, the 20-bit radius tail bound, and
+    replica / step streams that differ."""
+    z = O.device_normals(7, np.arange(0, 2000), 0, 64, 1.0)
+    assert abs(z.mean()) < 0.01 and abs(z.var() - 1.0) < 0.02
+    assert abs(np.mean(z ** 4) - 3.0) < 0.1          # Gaussian kurtosis
+    assert np.abs(z).max() <= np.sqrt(-2 * np.log(0.5 * 2.0 ** -20)) + 1e-12
+    z1 = O.device_normals(7, np.arange(0, 4), 1, 64, 1.0)
+    assert not np.allclose(z[:4], z1) and not np.allclose(z[0], z[1])
