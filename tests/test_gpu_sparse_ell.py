@@ -92,7 +92,7 @@ def _both(fn):
 
 
 @pytest.mark.parametrize("graph", sorted(GRAPHS))
-@pytest.mark.parametrize("R", [1, 37, 64, 300])
+@pytest.mark.parametrize("R", [1, 37, 64, 96, 300])  # 1 and 96: one replica per lane
 def test_ell_equals_csr_seeded(graph, R):
     p = GRAPHS[graph]()
     p.device_handle().set_path("sparse")
