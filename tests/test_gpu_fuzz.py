@@ -1,0 +1,83 @@
+"""Randomised parity sweep through the C ABI against the float64 oracle.
+
+Deterministic cases (seeded) over n in [1, 700], edge density, integer / real
+weights, fields, replica counts (partial blocks, one replica per lane) and
+every kernel path forced in turn, weight magnitudes that need the power-of-two
+J scale (|w| up to 5000) and tiny real weights. Injected noise makes the comparison
+per-trajectory; the criteria are the ragged-shape ones of test_gpu_parity.py
+(mean error, rare large deviations, rare sign flips) and exact energies for
+integer instances.
+"""
+
+import numpy as np
+import pytest
+
+import nmfa_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1806_08422_b200 as nb  # noqa: E402
+from paper_1806_08422_b200 import _native  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1806_08422_b200 import build
+    build.build()
+    _native.load()
+
+
+def make_case(k):
+    rng = np.random.default_rng(1000 + k)
+    n = int(rng.choice([1, 2, 3, 7, 8, 9, 31, 64, 100, 129, 200, 255, 256, 257, 300, 383, 511, 700]))
+    kind = rng.choice(["sparse", "mid", "dense"])
+    p_edge = {"sparse": min(1.0, 3.0 / max(n - 1, 1)), "mid": 0.1, "dense": 0.7}[kind]
+    i, j = np.triu_indices(n, 1)
+    keep = rng.random(i.size) < p_edge
+    i, j = i[keep], j[keep]
+    integer = bool(rng.integers(0, 2))
+    scale = rng.choice([1.0, 1.0, 5000.0, 1e-3])  # 5000: beyond fp16-exact integers -> j_scale
+    if integer:
+        top = 3 if scale != 5000.0 else 5000
+        w = rng.integers(-top, top + 1, i.size).astype(float)
+    else:
+        w = rng.normal(size=i.size) * scale
+    if integer:
+        nz = w != 0
+        i, j, w = i[nz], j[nz], w[nz]
+    h = None
+    if rng.random() < 0.5:
+        h = rng.integers(-2, 3, n).astype(float) if integer else rng.normal(scale=0.5, size=n)
+    R = int(rng.choice([1, 5, 33, 64, 96, 130]))
+    paths = ["dense", "sparse"] + (["small"] if n <= 256 else [])
+    path = str(rng.choice(paths))
+    return n, i, j, w, h, R, path, integer
+
+
+@pytest.mark.parametrize("k", range(96))
+def test_random_instance_matches_oracle(k):
+    n, i, j, w, h, R, path, integer = make_case(k)
+    p = nb.IsingProblem.from_arrays(n, i, j, w, h)
+    p.device_handle().set_path(path)
+    t_f = 24
+    temps = O.temperatures(t_f)
+    noise = np.random.default_rng(k).standard_normal((R, t_f, n)) * 0.15
+    S, _ = nb.run_with_noise(p, temps, noise, 0.15)
+    S = np.atleast_2d(S)
+    op = O.problem_from_edges(n, i, j, w, h)
+    ref = np.stack([O.anneal(op, np.zeros(n), temps, noise[r], 0.15)[0] for r in range(R)])
+    err = np.abs(S - ref)
+    info = f"case {k}: n={n} edges={len(i)} R={R} path={path} int={integer} h={h is not None}"
+    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= 2e-3, (info, err.mean(), err.max())
+    firm = np.abs(ref) > 2e-2
+    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= 2e-3, info
+    cfg = O.sign_round(S)
+    got, want = nb.energies(p, cfg), O.energies(op, cfg)
+    if integer:
+        assert np.array_equal(got, want), info
+    else:
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-9), info
