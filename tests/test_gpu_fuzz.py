@@ -81,3 +81,32 @@ def test_random_instance_matches_oracle(k):
         assert np.array_equal(got, want), info
     else:
         assert np.allclose(got, want, rtol=1e-12, atol=1e-9), info
+
+
+@pytest.mark.parametrize("k", range(24))
+def test_random_ground_state_matches_oracle(k):
+    """The GPU enumerator (brute_force_ground) against the oracle's chunked
+    enumeration on random small instances: +-1, small-integer and real weights,
+    with and without fields, n in [2, 16]. Energy, degeneracy (within the
+    reference's tie tolerance) and a minimising configuration."""
+    rng = np.random.default_rng(5000 + k)
+    n = int(rng.integers(2, 17))
+    i, j = np.triu_indices(n, 1)
+    keep = rng.random(i.size) < rng.choice([0.2, 0.5, 1.0])
+    i, j = i[keep], j[keep]
+    kind = k % 3
+    w = (np.where(rng.random(i.size) < 0.5, 1.0, -1.0) if kind == 0 else
+         rng.integers(-3, 4, i.size).astype(float) if kind == 1 else rng.normal(size=i.size))
+    nz = w != 0
+    i, j, w = i[nz], j[nz], w[nz]
+    h = None if rng.random() < 0.5 else (
+        rng.integers(-2, 3, n).astype(float) if kind < 2 else rng.normal(scale=0.5, size=n))
+    p = nb.IsingProblem.from_arrays(n, i, j, w, h)
+    gt, cfg = nb.brute_force_ground(p, return_config=True)
+    e, c = O.gray_ground(O.problem_from_edges(n, i, j, w, h))
+    info = f"case {k}: n={n} edges={len(i)} kind={kind} h={h is not None}"
+    if kind < 2:
+        assert (gt.energy, gt.degeneracy) == (e, c), (info, gt, e, c)
+    else:
+        assert abs(gt.energy - e) <= 1e-9 * max(1.0, abs(e)) and gt.degeneracy == c, (info, gt, e, c)
+    assert abs(O.energy(O.problem_from_edges(n, i, j, w, h), cfg) - gt.energy) <= 1e-9 * max(1.0, abs(e))
