@@ -472,3 +472,39 @@ def test_problem_without_couplers(path):
     res = nb.sample(p, nb.NmfaParams(t_f=50, seed=1), 128)
     cfg = res.configs.cpu().numpy().astype(np.float64)
     assert np.allclose(res.energies.cpu().numpy(), cfg @ h, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("path,make", [("small", lambda: nb.gen_sk(60, 1)),
+                                       ("dense", lambda: nb.gen_sk(300, 2)),
+                                       ("sparse", lambda: nb.moebius_ladder(520)),
+                                       ("sparse", lambda: nb.gen_dense_maxcut(400, 0.02, 1))])
+def test_plan_run_is_graph_capturable(path, make):
+    """nmfa_plan_run allocates nothing and only enqueues (include/nmfa_b200.h):
+    captured in a CUDA graph and replayed, it reproduces a direct run bitwise."""
+    p = make()
+    p.device_handle().set_path(path)
+    params = nb.NmfaParams(t_f=40, seed=9)
+    R = 96
+    plan = nb.Plan(p, R, params.schedule.temperatures(params.t_f), params.alpha, params.sigma)
+    cfg0 = torch.empty((R, p.n), dtype=torch.int8, device="cuda")
+    e0 = torch.empty(R, dtype=torch.float64, device="cuda")
+    plan.run(params.seed, 0, config=cfg0, energy=e0)
+    torch.cuda.synchronize()
+    cfg1 = torch.zeros_like(cfg0)
+    e1 = torch.zeros_like(e0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        plan.run(params.seed, 0, config=cfg1, energy=e1, stream=s)  # warm-up on the side stream
+        torch.cuda.synchronize()
+        cfg1.zero_()
+        e1.zero_()
+        with torch.cuda.graph(g, stream=s):
+            plan.run(params.seed, 0, config=cfg1, energy=e1, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        cfg1.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(cfg1, cfg0) and torch.equal(e1, e0)
