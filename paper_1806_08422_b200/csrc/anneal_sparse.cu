@@ -11,7 +11,9 @@
 // Measured design steps: profiles/r01/ell_notes.log, DESIGN.md section 6.
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -45,7 +47,7 @@ struct SparseStepArgs {
   int n, t, t_f;
   long long R, Rp;
   float inv_t, alpha, oma, sigma;
-  unsigned long long key_base;
+  const unsigned long long* key_base;  // device word, written per run (graph-stable args)
   const float* noise;  // [R][t_f][n] or null
   int8_t* cfg;         // written at the last step
   float* s_out;
@@ -102,7 +104,7 @@ __device__ __forceinline__ void sparse_noise(const SparseStepArgs& a, int q, int
         z[c][qq] = (valid && i < n) ? a.noise[((long long)rc * a.t_f + a.t) * n + i] : 0.f;
       }
     } else {
-      const unsigned long long key = a.key_base + (unsigned long long)rc;
+      const unsigned long long key = __ldg(a.key_base) + (unsigned long long)rc;
       normal8(philox_schedule((uint32_t)key, (uint32_t)(key >> 32)), (uint32_t)q, (uint32_t)a.t,
               bm_scale(a.sigma), z[c]);
     }
@@ -410,14 +412,58 @@ static bool ell_disabled() {
   return e && e[0] == '1';
 }
 
-int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+// Per-plan launch state.  The t_f step launches of a run differ from run to
+// run only in the Philox key base (a device word, written by a one-thread
+// kernel), the initial state s0 (init node) and the outputs written at the
+// last step (last node).  So the init + t_f steps are built once as a CUDA
+// graph and replayed: about 2.7 us less per step than stream launches
+// (cubic n = 512: 6.35 -> 3.62 us/step; profiles/r01/ell_notes.log).  Runs
+// with injected noise or a trajectory record, runs on a stream that is itself
+// being captured, and NMFA_SPARSE_GRAPH=0 launch the same kernels directly.
+struct SparseGraph {
+  unsigned long long* d_key = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t init_node = nullptr, last_node = nullptr;
+  std::string signature;  // kernel variant + launch geometry the graph holds
+  const float* s0 = nullptr;
+  int8_t* cfg = nullptr;
+  float* s_out = nullptr;
+};
+
+void sparse_plan_free(nmfa_plan* pl) {
+  auto* g = static_cast<SparseGraph*>(pl->sparse);
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  if (g->d_key) cudaFree(g->d_key);
+  delete g;
+  pl->sparse = nullptr;
+}
+
+__global__ void sparse_set_key_kernel(unsigned long long* d, unsigned long long v) { *d = v; }
+
+int launch_sparse_anneal(nmfa_plan* pl, uint64_t key_base, const float* noise,
                          const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                          cudaStream_t st) {
   const nmfa_problem* p = pl->p;
-  const long long tot = (long long)p->n * pl->Rp;
-  sparse_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_sa, s0, (int)p->n,
-                                                                     pl->R, pl->Rp);
+  if ((long long)p->n * pl->Rp >= (1LL << 31) || (p->n + 7) / 8 > 65535) {
+    set_error("sparse path: needs n <= 524280 and n x padded replicas < 2^31 per plan");
+    return NMFA_ERR_ARG;
+  }
+  if (!pl->sparse) {
+    auto* g = new SparseGraph();
+    if (cudaMalloc(&g->d_key, sizeof(unsigned long long)) != cudaSuccess) {
+      delete g;
+      set_error("out of device memory for the sparse plan");
+      return NMFA_ERR_CUDA;
+    }
+    pl->sparse = g;
+  }
+  auto* G = static_cast<SparseGraph*>(pl->sparse);
+  sparse_set_key_kernel<<<1, 1, 0, st>>>(G->d_key, (unsigned long long)key_base);
   NMFA_LAUNCH_CHECK();
+
   const std::vector<float>& inv_t = pl->h_inv_temp;
   SparseStepArgs a{};
   a.ptr = p->d_csr_ptr;
@@ -432,16 +478,12 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   a.alpha = pl->alpha;
   a.oma = pl->oma;
   a.sigma = pl->sigma;
-  a.key_base = key_base;
+  a.key_base = G->d_key;
   a.elem_bytes = (uint32_t)sizeof(float);
   a.noise = noise;
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
-  if ((long long)p->n * pl->Rp >= (1LL << 31) || (p->n + 7) / 8 > 65535) {
-    set_error("sparse path: needs n <= 524280 and n x padded replicas < 2^31 per plan");
-    return NMFA_ERR_ARG;
-  }
   // two replicas per lane whenever the padded replica count allows (Rp % 64 == 0)
   const char* v_env = getenv("NMFA_SPARSE_V");  // A/B: "1" forces one replica per lane
   const bool v2 = pl->Rp % 64 == 0 && !(v_env && v_env[0] == '1');
@@ -468,30 +510,118 @@ int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* no
   const long long strips = (n_groups + a.groups_per_warp - 1) / a.groups_per_warp;
   const dim3 grid_ell((unsigned)((strips + strips_per_block - 1) / strips_per_block),
                       (unsigned)((n_slices + a.slices_per_block - 1) / a.slices_per_block));
-  float* cur = pl->d_sa;
-  float* nxt = pl->d_sb;
-  for (int t = 0; t < pl->t_f; ++t) {
-    a.t = t;
-    a.inv_t = inv_t[t];
-    a.last = (t == pl->t_f - 1);
-    a.s_old = cur;
-    a.s_new = nxt;
-    if (ell_k == 3 && v2)
-      sparse_ell_kernel<2, 3><<<grid_ell, 256, 0, st>>>(a);
-    else if (ell_k == 3)
-      sparse_ell_kernel<1, 3><<<grid_ell, 256, 0, st>>>(a);
-    else if (ell_k == 4 && v2)
-      sparse_ell_kernel<2, 4><<<grid_ell, 256, 0, st>>>(a);
-    else if (ell_k == 4)
-      sparse_ell_kernel<1, 4><<<grid_ell, 256, 0, st>>>(a);
-    else if (v2)
-      sparse_step_kernel<2><<<grid, 256, 0, st>>>(a);
-    else
-      sparse_step_kernel<1><<<grid, 256, 0, st>>>(a);
-    NMFA_LAUNCH_CHECK();
-    std::swap(cur, nxt);
+  void* kern;
+  dim3 kgrid = grid_ell;
+  if (ell_k == 3 && v2)
+    kern = (void*)sparse_ell_kernel<2, 3>;
+  else if (ell_k == 3)
+    kern = (void*)sparse_ell_kernel<1, 3>;
+  else if (ell_k == 4 && v2)
+    kern = (void*)sparse_ell_kernel<2, 4>;
+  else if (ell_k == 4)
+    kern = (void*)sparse_ell_kernel<1, 4>;
+  else {
+    kern = v2 ? (void*)sparse_step_kernel<2> : (void*)sparse_step_kernel<1>;
+    kgrid = grid;
   }
-  add_launches(1 + pl->t_f);
+  const long long tot = (long long)p->n * pl->Rp;
+  const dim3 init_grid((unsigned)((tot + 255) / 256));
+  int n_i = (int)p->n;
+  long long R = pl->R, Rp = pl->Rp;
+  float* d_sa = pl->d_sa;
+  add_launches(2 + pl->t_f);
+
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  const char* g_env = getenv("NMFA_SPARSE_GRAPH");
+  const bool direct = noise || s_hist || cap != cudaStreamCaptureStatusNone ||
+                      (g_env && g_env[0] == '0');
+  if (direct) {
+    sparse_init_kernel<<<init_grid, 256, 0, st>>>(d_sa, s0, n_i, R, Rp);
+    NMFA_LAUNCH_CHECK();
+    float* cur = pl->d_sa;
+    float* nxt = pl->d_sb;
+    for (int t = 0; t < pl->t_f; ++t) {
+      a.t = t;
+      a.inv_t = inv_t[t];
+      a.last = (t == pl->t_f - 1);
+      a.s_old = cur;
+      a.s_new = nxt;
+      void* args[] = {&a};
+      NMFA_CUDA_TRY(cudaLaunchKernel(kern, kgrid, dim3(256), args, 0, st));
+      std::swap(cur, nxt);
+    }
+    return NMFA_OK;
+  }
+
+  char sig[256];
+  snprintf(sig, sizeof(sig), "%p %u %u %d %d %d", kern, kgrid.x, kgrid.y, a.groups_per_warp,
+           a.slices_per_block, pl->t_f);
+  if (!G->exec || G->signature != sig) {
+    if (G->exec) cudaGraphExecDestroy(G->exec);
+    if (G->graph) cudaGraphDestroy(G->graph);
+    G->exec = nullptr;
+    G->graph = nullptr;
+    NMFA_CUDA_TRY(cudaGraphCreate(&G->graph, 0));
+    cudaKernelNodeParams kp{};
+    void* init_args[] = {&d_sa, (void*)&s0, &n_i, &R, &Rp};
+    kp.func = (void*)sparse_init_kernel;
+    kp.gridDim = init_grid;
+    kp.blockDim = dim3(256);
+    kp.kernelParams = init_args;
+    NMFA_CUDA_TRY(cudaGraphAddKernelNode(&G->init_node, G->graph, nullptr, 0, &kp));
+    cudaGraphNode_t prev_node = G->init_node;
+    float* cur = pl->d_sa;
+    float* nxt = pl->d_sb;
+    for (int t = 0; t < pl->t_f; ++t) {
+      a.t = t;
+      a.inv_t = inv_t[t];
+      a.last = (t == pl->t_f - 1);
+      a.s_old = cur;
+      a.s_new = nxt;
+      void* args[] = {&a};
+      kp.func = kern;
+      kp.gridDim = kgrid;
+      kp.kernelParams = args;
+      cudaGraphNode_t node;
+      NMFA_CUDA_TRY(cudaGraphAddKernelNode(&node, G->graph, &prev_node, 1, &kp));
+      prev_node = node;
+      std::swap(cur, nxt);
+    }
+    G->last_node = prev_node;
+    NMFA_CUDA_TRY(cudaGraphInstantiate(&G->exec, G->graph, 0));
+    G->signature = sig;
+    G->s0 = s0;
+    G->cfg = cfg;
+    G->s_out = s_out;
+  }
+  if (G->s0 != s0) {  // re-point the init node
+    cudaKernelNodeParams kp{};
+    void* init_args[] = {&d_sa, (void*)&s0, &n_i, &R, &Rp};
+    kp.func = (void*)sparse_init_kernel;
+    kp.gridDim = init_grid;
+    kp.blockDim = dim3(256);
+    kp.kernelParams = init_args;
+    NMFA_CUDA_TRY(cudaGraphExecKernelNodeSetParams(G->exec, G->init_node, &kp));
+    G->s0 = s0;
+  }
+  if (G->cfg != cfg || G->s_out != s_out) {  // re-point the last step's outputs
+    a.t = pl->t_f - 1;
+    a.inv_t = inv_t[pl->t_f - 1];
+    a.last = 1;
+    a.s_old = (pl->t_f - 1) % 2 == 0 ? pl->d_sa : pl->d_sb;
+    a.s_new = (pl->t_f - 1) % 2 == 0 ? pl->d_sb : pl->d_sa;
+    void* args[] = {&a};
+    cudaKernelNodeParams kp{};
+    kp.func = kern;
+    kp.gridDim = kgrid;
+    kp.blockDim = dim3(256);
+    kp.kernelParams = args;
+    NMFA_CUDA_TRY(cudaGraphExecKernelNodeSetParams(G->exec, G->last_node, &kp));
+    G->cfg = cfg;
+    G->s_out = s_out;
+  }
+  NMFA_CUDA_TRY(cudaGraphLaunch(G->exec, st));
   return NMFA_OK;
 }
 

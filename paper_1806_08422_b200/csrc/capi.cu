@@ -531,6 +531,7 @@ int nmfa_plan_destroy(nmfa_plan_t* pl) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   dense_plan_free(pl);
+  sparse_plan_free(pl);
   cudaSetDevice(prev);
   delete pl;
   return NMFA_OK;

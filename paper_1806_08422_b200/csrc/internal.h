@@ -109,6 +109,7 @@ struct nmfa_plan {
   int8_t* d_hist_cfg = nullptr; // trajectory energies: signs of s_hist
   int64_t bits_words = 0;       // capacity of d_bits in uint32
   void* dense = nullptr;        // DenseState (anneal_dense.cu)
+  void* sparse = nullptr;       // SparseGraph (anneal_sparse.cu): captured step graph
 };
 
 namespace nmfa {
@@ -116,9 +117,10 @@ namespace nmfa {
 int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         cudaStream_t st);
-int launch_sparse_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
+int launch_sparse_anneal(nmfa_plan* pl, uint64_t key_base, const float* noise,
                          const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                          cudaStream_t st);
+void sparse_plan_free(nmfa_plan* pl);
 int launch_dense_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,
                         double* energy, bool* energy_done, cudaStream_t st);

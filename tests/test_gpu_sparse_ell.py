@@ -173,3 +173,43 @@ def test_energy_field_term_in_chunks(integer_h):
         assert np.array_equal(got, want)
     else:
         assert np.allclose(got, want, rtol=1e-12, atol=1e-9)
+
+
+def test_graph_replay_equals_direct_launches():
+    """The sparse path replays its t_f steps from a per-plan CUDA graph; the key
+    base, s0 and the last step's outputs change per run (init / last node
+    re-pointed). Runs of one plan with changing seeds, outputs and s0 must equal
+    direct stream launches (NMFA_SPARSE_GRAPH=0) bit for bit."""
+    p = nb.gen_cubic_maxcut(300, 3)
+    p.device_handle().set_path("sparse")
+    params = nb.NmfaParams(t_f=50, seed=1)
+    R = 128
+    plan = nb.Plan(p, R, params.schedule.temperatures(params.t_f), params.alpha, params.sigma)
+    s0 = torch.as_tensor(np.random.default_rng(0).uniform(-0.5, 0.5, (R, p.n)),
+                         dtype=torch.float32, device="cuda")
+    runs = [(1, None), (2, s0), (1, None), (3, s0), (3, None)]
+
+    def go():
+        outs = []
+        for seed, init in runs:
+            cfg = torch.empty((R, p.n), dtype=torch.int8, device="cuda")  # fresh buffers
+            sf = torch.empty((R, p.n), dtype=torch.float32, device="cuda")
+            plan.run(seed, 0, s0=init, config=cfg, s_final=sf)
+            torch.cuda.synchronize()
+            outs.append((cfg.cpu(), sf.cpu()))
+        return outs
+
+    old = os.environ.get("NMFA_SPARSE_GRAPH")
+    try:
+        os.environ["NMFA_SPARSE_GRAPH"] = "1"
+        graph = go()
+        os.environ["NMFA_SPARSE_GRAPH"] = "0"
+        direct = go()
+    finally:
+        if old is None:
+            os.environ.pop("NMFA_SPARSE_GRAPH", None)
+        else:
+            os.environ["NMFA_SPARSE_GRAPH"] = old
+    for (c1, s1), (c2, s2) in zip(graph, direct):
+        assert torch.equal(c1, c2) and torch.equal(s1, s2)
+    assert torch.equal(graph[0][0], graph[2][0]) and not torch.equal(graph[0][0], graph[1][0])
