@@ -2,6 +2,7 @@
 final-sign flips against the float64 oracle when the J.s operand is quantized.
 Same setup as tests/test_gpu_parity.py::test_dense_large_injected_noise_matches_oracle
 (gen_sk(520, 5), t_f=120, R=300, injected noise sigma=0.15). Modes:
+  bf16      : s -> bf16(s)                          (the north star's "S in bf16")
   f16       : s -> fp16(s)                          (today's operand)
   f16hilo   : fp16(s) + fp16(s - fp16(s))           (hi+lo both as operands)
   fixK      : s -> round(s * 2^K) / 2^K             (fixed point, K fractional bits)
@@ -42,7 +43,15 @@ def run(q, th=np.tanh):
 
 
 ref = run(lambda s: s)
-modes = {"f16": lambda s: s.astype(np.float16).astype(np.float64),
+def bf16(x):
+    """round-to-nearest-even to bfloat16 (8-bit significand)"""
+    b = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+modes = {"bf16": bf16,
+         "f16": lambda s: s.astype(np.float16).astype(np.float64),
          "f16hilo": lambda s: (lambda h: h + (s - h).astype(np.float16).astype(np.float64))(
              s.astype(np.float16).astype(np.float64))}
 for K in (11, 13, 14, 15, 16, 20):
