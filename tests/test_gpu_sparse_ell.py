@@ -213,3 +213,18 @@ def test_graph_replay_equals_direct_launches():
     for (c1, s1), (c2, s2) in zip(graph, direct):
         assert torch.equal(c1, c2) and torch.equal(s1, s2)
     assert torch.equal(graph[0][0], graph[2][0]) and not torch.equal(graph[0][0], graph[1][0])
+
+
+def test_sample_many_on_the_sparse_path_equals_single_runs():
+    """nmfa_anneal_many with instances above the small-path size loops over the
+    per-problem plans (sparse graph replay here); each instance must equal its
+    own sample() call with the bench-loop seed."""
+    from dataclasses import replace
+    probs = [nb.gen_cubic_maxcut(400, s) for s in range(3)] + [mixed(400, 9)]
+    params = nb.NmfaParams(t_f=40, seed=21)
+    R = 64
+    cfg, en, _ = nb.sample_many(probs, params, R)
+    for k, p in enumerate(probs):
+        assert p.device_info()["path"] == "sparse"
+        one = nb.sample(p, replace(params, seed=params.seed + k * R), R)
+        assert torch.equal(cfg[k], one.configs) and torch.equal(en[k], one.energies)
