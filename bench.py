@@ -9,7 +9,7 @@ sharded with no data-path collective; one all-gather of each rank's best at
 the end).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload k2000|sk100|moebius100|g2000|moebius131072|ground26|sk65536]
+                    [--workload k2000|sk100|moebius100|g2000|moebius131072|torus|ground26|sk65536]
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle port
 of the reference's per-run loop (oracle/nmfa_oracle.py, which follows
@@ -41,6 +41,9 @@ WORKLOADS = {
     # the sparse path where it is the routed one (large, low-degree instance: ELL kernel)
     "moebius131072": ("moebius_ladder(131072)", 131072, 1024, 200,
                       "Moebius ladder n=131072 (sparse ELL path), 1024 reads/GPU, t_f=200"),
+    # the G-set toroidal class at scale (degree 4: ELL kernel with 4 slots)
+    "torus": ("toroidal_grid(362, 362, 1)", 131044, 1024, 200,
+              "toroidal grid 362x362 (n=131044, +-1 couplers, sparse ELL path), 1024 reads/GPU, t_f=200"),
     # exhaustive ground state (brute_force_ground) at the reference's limit
     "ground26": ("gen_sk(26, 1)", 26, 1, 1, "exact ground state of gen_sk(26,1) by Gray-code enumeration"),
     # config 5: J generated on device, row-sharded over the ranks (strong scaling)
@@ -159,7 +162,7 @@ def cpu_reference(workload, sample_runs=None, threads=None):
     threads = threads or os.cpu_count() or 1
     if sample_runs is None:
         sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads,
-                       "moebius131072": threads}.get(workload, 64 * threads)
+                       "moebius131072": threads, "torus": threads}.get(workload, 64 * threads)
     O.batch(op, 10**6, threads, t_f=20, threads=threads)  # warm BLAS / thread pool
     t0 = time.perf_counter()
     _, e = O.batch(op, 0, sample_runs, t_f=t_f, threads=threads)

@@ -134,3 +134,17 @@ def test_accepts_reference_like_objects():
         h = np.zeros(3)
     p = nb.as_problem(Ref())
     assert isinstance(p, nb.IsingProblem) and p.num_edges == 2
+
+
+def test_toroidal_grid_generator():
+    """toroidal_grid: every spin has degree 4, 2*rows*cols couplers of +-1,
+    deterministic in the seed (the torus bench workload)."""
+    import paper_1806_08422_b200 as nb
+    p = nb.toroidal_grid(7, 5, 3)
+    deg = np.bincount(np.concatenate([p.edges_i, p.edges_j]), minlength=p.n)
+    assert p.n == 35 and p.num_edges == 70 and np.all(deg == 4)
+    assert set(np.unique(p.edge_weights)) <= {-1.0, 1.0}
+    q = nb.toroidal_grid(7, 5, 3)
+    assert np.array_equal(p.edge_weights, q.edge_weights)
+    with pytest.raises(ValueError):
+        nb.toroidal_grid(2, 5, 0)

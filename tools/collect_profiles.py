@@ -4,7 +4,7 @@ import json, os, shutil, subprocess, sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(REPO, "gpurun_out"), os.path.join(REPO, "profiles", "r01")
-for f in ["bench_k2000", "bench_moebius131072", "bench_sk100", "bench_g2000", "bench_moebius100",
+for f in ["bench_k2000", "bench_moebius131072", "bench_torus", "bench_sk100", "bench_g2000", "bench_moebius100",
           "bench_ground26", "bench_sk65536_g1"]:
     src = os.path.join(G, f + ".json")
     if os.path.exists(src):

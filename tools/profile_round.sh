@@ -6,6 +6,7 @@ python bench.py > gpurun_out/bench_k2000.json 2> gpurun_out/bench_k2000.err; tai
 python bench.py --workload moebius131072 --steps 5 --warmup 3 --no-tts > gpurun_out/bench_moebius131072.json 2> gpurun_out/bench_m.err
 python bench.py --workload sk100 --steps 5 --warmup 3 --no-tts --no-cpu-baseline > gpurun_out/bench_sk100.json 2> gpurun_out/bench_s.err
 python bench.py --workload g2000 --steps 5 --warmup 3 --no-tts --no-cpu-baseline > gpurun_out/bench_g2000.json 2> gpurun_out/bench_g.err
+python bench.py --workload torus --steps 5 --warmup 3 --no-tts > gpurun_out/bench_torus.json 2> gpurun_out/bench_t.err
 python bench.py --workload moebius100 --steps 5 --warmup 3 --no-tts --no-cpu-baseline > gpurun_out/bench_moebius100.json 2> gpurun_out/bench_m100.err
 python bench.py --workload ground26 --steps 5 --warmup 3 > gpurun_out/bench_ground26.json 2> gpurun_out/bench_gr.err
 python bench.py --workload sk65536 --steps 2 --warmup 1 > gpurun_out/bench_sk65536_g1.json 2> gpurun_out/bench_sk.err
