@@ -22,6 +22,9 @@
 #ifndef NMFA_CSR_ROUNDS
 #define NMFA_CSR_ROUNDS 2
 #endif
+#ifndef NMFA_ELL4_MINB
+#define NMFA_ELL4_MINB 2  // the degree-4 ELL variant (A/B knob)
+#endif
 #ifndef NMFA_ELL_MINB
 #define NMFA_ELL_MINB 2  // ELL kernel blocks per SM (128 registers, no spill at V = 2)
 #endif
@@ -317,7 +320,8 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
 // 8K (index, weight) slots loaded while the current group's gathers are in
 // flight, so one memory round trip per group remains on the critical path.
 template <int V, int K>
-__global__ void __launch_bounds__(256, NMFA_ELL_MINB) sparse_ell_kernel(const SparseStepArgs a) {
+__global__ void __launch_bounds__(256, K == 4 ? NMFA_ELL4_MINB : NMFA_ELL_MINB)
+    sparse_ell_kernel(const SparseStepArgs a) {
   using Vec = typename std::conditional<V == 2, float2, float>::type;
   static_assert(8 * K <= 32, "one slot per lane");
   // grid (spin strips, replica slices), strips fastest.  A block's 8 warps
