@@ -22,6 +22,9 @@
 #ifndef NMFA_CSR_ROUNDS
 #define NMFA_CSR_ROUNDS 2
 #endif
+#ifndef NMFA_ELL_FULL_GROUPS
+#define NMFA_ELL_FULL_GROUPS 1  // unpredicated state loads for interior groups (+1-1.5%, no spill)
+#endif
 #ifndef NMFA_ELL4_MINB
 #define NMFA_ELL4_MINB 2  // the degree-4 ELL variant (A/B knob)
 #endif
@@ -352,13 +355,21 @@ __global__ void __launch_bounds__(256, K == 4 ? NMFA_ELL4_MINB : NMFA_ELL_MINB)
   const bool slot = lane < 8 * K;
   auto issue = [&](int q, int off_l, float (&sold)[8][V], float (&v)[8][K][V]) {
     const int i_base = 8 * q;
+#if NMFA_ELL_FULL_GROUPS
+    if (i_base + 8 <= n) {  // interior group: no per-spin bounds checks
 #pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      if (i_base + qq < n) {
-        ld((i_base + qq) * Rp, sold[qq]);
-      } else {
+      for (int qq = 0; qq < 8; ++qq) ld((i_base + qq) * Rp, sold[qq]);
+    } else
+#endif
+    {
 #pragma unroll
-        for (int c = 0; c < V; ++c) sold[qq][c] = 0.f;
+      for (int qq = 0; qq < 8; ++qq) {
+        if (i_base + qq < n) {
+          ld((i_base + qq) * Rp, sold[qq]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < V; ++c) sold[qq][c] = 0.f;
+        }
       }
     }
 #pragma unroll
