@@ -22,6 +22,9 @@
 #ifndef NMFA_CSR_ROUNDS
 #define NMFA_CSR_ROUNDS 2
 #endif
+#ifndef NMFA_FULL_GROUP_STORES
+#define NMFA_FULL_GROUP_STORES 1  // unpredicated state stores for interior groups (+1%)
+#endif
 #ifndef NMFA_ELL_FULL_GROUPS
 #define NMFA_ELL_FULL_GROUPS 1  // unpredicated state loads for interior groups (+1-1.5%, no spill)
 #endif
@@ -156,14 +159,24 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
       }
     }
   }
-#pragma unroll
-  for (int qq = 0; qq < 8; ++qq) {
+  auto store = [&](int qq) {
     const int i = i_base + qq;
-    if (i >= n) break;
     if constexpr (V == 2)
       st_global_v2(elem_addr<kImad>(sn, i * Rp, a.elem_bytes), acc[qq][0], acc[qq][1]);
     else
       st_global(elem_addr<kImad>(sn, i * Rp, a.elem_bytes), acc[qq][0]);
+  };
+#if NMFA_FULL_GROUP_STORES
+  if (i_base + 8 <= n) {  // interior group: no per-spin bounds checks
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) store(qq);
+    return;
+  }
+#endif
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    if (i_base + qq >= n) break;
+    store(qq);
   }
 }
 
