@@ -110,3 +110,43 @@ def test_random_ground_state_matches_oracle(k):
     else:
         assert abs(gt.energy - e) <= 1e-9 * max(1.0, abs(e)) and gt.degeneracy == c, (info, gt, e, c)
     assert abs(O.energy(O.problem_from_edges(n, i, j, w, h), cfg) - gt.energy) <= 1e-9 * max(1.0, abs(e))
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_random_large_instance_matches_oracle(k):
+    """Multi-tile shapes: n in [700, 3000] (ragged last tiles of the dense
+    kernel, partial spin groups of the sparse ones), random density and weights,
+    R up to 257, against the replica-batched float64 oracle."""
+    rng = np.random.default_rng(9000 + k)
+    n = int(rng.integers(700, 3001))
+    density = float(rng.choice([3.0 / n, 0.02, 0.3, 1.0]))
+    m = int(density * n * (n - 1) / 2)
+    a, b = rng.integers(0, n, 2 * m + 16), rng.integers(0, n, 2 * m + 16)
+    keep = a != b
+    key = np.unique(np.minimum(a, b)[keep] * n + np.maximum(a, b)[keep])[:max(m, 1)]
+    i, j = key // n, key % n
+    integer = bool(k % 2)
+    w = np.where(rng.random(i.size) < 0.5, 1.0, -1.0) if integer else rng.normal(size=i.size)
+    h = rng.integers(-1, 2, n).astype(float) if (integer and k % 4 == 1) else None
+    R = int(rng.choice([8, 64, 257]))
+    path = "dense" if k % 3 != 2 else "sparse"
+    p = nb.IsingProblem.from_arrays(n, i, j, w, h)
+    p.device_handle().set_path(path)
+    t_f = 24
+    temps = O.temperatures(t_f)
+    noise = np.random.default_rng(k).standard_normal((R, t_f, n)) * 0.15
+    S, _ = nb.run_with_noise(p, temps, noise, 0.15)
+    S = np.atleast_2d(S)
+    op = O.problem_from_edges(n, i, j, w, h)
+    ref = O.batched_anneal(op, None, t_f=t_f, temps=temps, noise=noise)
+    err = np.abs(S - ref)
+    info = f"case {k}: n={n} edges={len(i)} R={R} path={path} int={integer}"
+    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= 2e-3, (info, err.mean(), err.max())
+    firm = np.abs(ref) > 2e-2
+    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= 2e-3, info
+    cfg = O.sign_round(S)
+    got, want = nb.energies(p, cfg), O.energies(op, cfg)
+    if integer:
+        assert np.array_equal(got, want), info
+    else:
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-9), info
