@@ -37,6 +37,7 @@
 // Experiment switches (measurements in profiles/r01/, none changes results
 // unless noted):
 //   env NMFA_TILE_ORDER = mmajor | sorted | spin | block | alt | rev  (tile dealing)
+//   env NMFA_KORDER = rotate   (tile starts at its own spin range's k-slice; timing only)
 //   env NMFA_KORDER = early    (earliest-published-slice-first K order; results
 //                               then depend on the schedule)
 //   env NMFA_TILE_W = 1..16    (force the tile width in 16-spin units)
@@ -918,6 +919,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   const int kbn = ds->kblocks;
   static const char* korder_env = getenv("NMFA_KORDER");
   const bool early = korder_env && std::string(korder_env) == "early";
+  // debug knob NMFA_KORDER=rotate: tile j starts at its own spin range's k-slice
+  // (spreads the concurrent reads of tiles that share A/J lines; timing only)
+  const bool rotate = korder_env && std::string(korder_env) == "rotate";
   std::vector<int> avail((size_t)mb * kbn, 0);
   for (int q = 0; q < pairs; ++q)
     for (int j = off[q]; j < off[q + 1]; ++j) {
@@ -926,10 +930,17 @@ int dense_plan_alloc(nmfa_plan* pl) {
         avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
     }
   std::vector<int16_t> korder;
-  if (early) korder.resize((size_t)T * kbn);
+  if (early || rotate) korder.resize((size_t)T * kbn);
   for (long long j = 0; j < T; ++j) {
     DenseTile& t = tiles[j];
     t.pad = kbn - 1;  // position of the short last k-slice in the tile's K order
+    if (rotate) {
+      int16_t* ko = &korder[(size_t)j * kbn];
+      const int s0 = ((t.n0 - (int)p->row_lo) >> 7) % kbn;
+      for (int k = 0; k < kbn; ++k) ko[k] = (int16_t)((k + s0) % kbn);
+      t.pad = (kbn - 1 - s0 + kbn) % kbn;
+      continue;
+    }
     if (!early) continue;
     int16_t* ko = &korder[(size_t)j * kbn];
     for (int k = 0; k < kbn; ++k) ko[k] = (int16_t)k;
@@ -939,7 +950,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
     for (int k = 0; k < kbn; ++k)
       if (ko[k] == kbn - 1) t.pad = k;
   }
-  if (early) {
+  if (early || rotate) {
     NMFA_CUDA_TRY(cudaMalloc(&ds->d_korder, korder.size() * sizeof(int16_t)));
     NMFA_CUDA_TRY(cudaMemcpy(ds->d_korder, korder.data(), korder.size() * sizeof(int16_t),
                              cudaMemcpyHostToDevice));
