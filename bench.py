@@ -53,6 +53,13 @@ WORKLOADS = {
 }
 
 
+DTYPES = {
+    "dense": "f16 operand / f16 hi+lo state (~22-bit) / f32 accumulate",
+    "small": "f16 operand / f32 state / f32 accumulate",
+    "sparse": "f32 state / f32 accumulate",
+}
+
+
 def metric_name(workload):
     return ("spin-updates/s (N*reads*steps/s) on K2000" if workload == "k2000"
             else f"spin-updates/s (N*reads*steps/s) on {workload}")
@@ -148,30 +155,67 @@ def dist_init():
     return world, rank, local
 
 
+def reference_package():
+    """The UNMODIFIED reference package installed into baseline/_ref (pip
+    --target), or None when it is absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "nmfa", "solver.py")):
+        return None
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")      # SURVEY Appendix B.7
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nmfa_ref_numba_cache")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import nmfa
+    except Exception:  # pragma: no cover - broken install: fall back to the port
+        return None
+    return nmfa
+
+
 def cpu_reference(workload, sample_runs=None, threads=None):
-    """Time the oracle port of the reference loop on a bounded sample (host cores)."""
+    """Time the reference's own per-run loop on a bounded sample (host cores).
+
+    Preferred: the installed reference itself, `nmfa.nmfa_batch(problem,
+    NmfaParams(t_f, seed=0), runs, threads)` with OPENBLAS_NUM_THREADS=1
+    (solver.py:262-280; kind "reference").  Fallback when baseline/_ref is
+    missing: the oracle's jitted restatement of the same loop (kind "port",
+    bit-exact with the reference's seeded energies, tests/test_oracle.py)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import nmfa_oracle as O
+    import numpy as np
 
     import paper_1806_08422_b200.instances as inst  # input construction only
 
     _, n, _, t_f, _ = WORKLOADS[workload]
     p = build_problem(inst, workload)
-    op = O.problem_from_edges(p.n, p.edges_i, p.edges_j, p.edge_weights, p.h)
     threads = threads or os.cpu_count() or 1
     if sample_runs is None:
         sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads,
                        "moebius131072": threads, "torus": threads}.get(workload, 64 * threads)
-    O.batch(op, 10**6, threads, t_f=20, threads=threads)  # warm BLAS / thread pool
-    t0 = time.perf_counter()
-    _, e = O.batch(op, 0, sample_runs, t_f=t_f, threads=threads)
-    wall = time.perf_counter() - t0
+    nmfa = reference_package()
+    if nmfa is not None:
+        cpl = np.column_stack([p.edges_i, p.edges_j, p.edge_weights])
+        rp = nmfa.IsingProblem(p.n, cpl, h=np.asarray(p.h, dtype=np.float64))
+        nmfa.nmfa_batch(rp, nmfa.NmfaParams(t_f=20, seed=10**6), threads, threads=threads)  # jit
+        t0 = time.perf_counter()
+        res = nmfa.nmfa_batch(rp, nmfa.NmfaParams(t_f=t_f, seed=0), sample_runs, threads=threads)
+        wall = time.perf_counter() - t0
+        best = min(r.final_energy for r in res)
+        kind, what = "reference", (f"the reference's nmfa.nmfa_batch (baseline/_ref, backend "
+                                   f"{nmfa.kernels.BACKEND}, OPENBLAS_NUM_THREADS=1)")
+    else:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import nmfa_oracle as O
+        op = O.problem_from_edges(p.n, p.edges_i, p.edges_j, p.edge_weights, p.h)
+        O.batch(op, 10**6, threads, t_f=20, threads=threads)  # warm BLAS / thread pool
+        t0 = time.perf_counter()
+        _, e = O.batch(op, 0, sample_runs, t_f=t_f, threads=threads)
+        wall = time.perf_counter() - t0
+        best = float(e.min())
+        kind, what = "port", "oracle per-run float64 loop (dgemv/CSR, numpy Philox noise)"
     return {"value": n * sample_runs * t_f / wall, "unit": "spin-updates/s", "cores": threads,
-            "kind": "port",
-            "sample": f"{sample_runs} runs x t_f={t_f} of the {workload} instance, oracle per-run "
-                      f"float64 loop (dgemv/CSR, numpy Philox noise), {threads} threads, "
-                      f"{wall:.1f} s wall, best E={e.min():.0f}",
+            "kind": kind,
+            "sample": f"{sample_runs} runs x t_f={t_f} of the {workload} instance, {what}, "
+                      f"{threads} threads, {wall:.1f} s wall, best E={best:.0f}",
             "wall_s": wall}
 
 
@@ -203,30 +247,116 @@ def measure_tts_sk100(nb, dev, skip_cpu=False):
     k = int(np.count_nonzero(e <= e_ref + 1e-9))
     pg = k / R
     tau = wall / R
-    out = {"instance": "gen_sk(100,0), t_f=1000, E_ref=-730 (best of 10k reference runs)",
+    out = {"instance": "gen_sk(100,0), t_f=1000, E_ref=-730 (best of 65,536 reference runs)",
            "gpu": {"reads": R, "p": pg, "tau_s": tau,
                    "tts99_s": tau * math.log(0.01) / math.log(1 - pg) if 0 < pg < 0.99 else None}}
     try:
-        golden = np.load(os.path.join(REPO, "tests", "golden", "stats.npz"))
+        golden = np.load(REF_STATS)
         pref = float(np.mean(golden["sk100_E"] <= e_ref + 1e-9))
         out["reference_p"] = pref
+        out["reference_reads"] = int(golden["sk100_E"].size)
     except OSError:
         pref = None
     if not skip_cpu and pref:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        sys.path.insert(0, os.path.join(REPO, "oracle"))
-        import nmfa_oracle as O
-
-        op = O.problem_from_edges(100, p.edges_i, p.edges_j, p.edge_weights)
         threads = os.cpu_count() or 1
-        O.batch(op, 0, threads, t_f=50, threads=threads)
         runs = 32 * threads
-        t0 = time.perf_counter()
-        O.batch(op, 0, runs, t_f=1000, threads=threads)
+        nmfa = reference_package()
+        if nmfa is not None:     # the installed reference itself
+            rp = nmfa.gen_sk(100, 0)
+            nmfa.nmfa_batch(rp, nmfa.NmfaParams(t_f=50, seed=0), threads, threads=threads)
+            t0 = time.perf_counter()
+            nmfa.nmfa_batch(rp, nmfa.NmfaParams(t_f=1000, seed=0), runs, threads=threads)
+            kind = "reference"
+        else:
+            sys.path.insert(0, os.path.join(REPO, "oracle"))
+            import nmfa_oracle as O
+            op = O.problem_from_edges(100, p.edges_i, p.edges_j, p.edge_weights)
+            O.batch(op, 0, threads, t_f=50, threads=threads)
+            t0 = time.perf_counter()
+            O.batch(op, 0, runs, t_f=1000, threads=threads)
+            kind = "port"
         tau_c = (time.perf_counter() - t0) / runs
         out["cpu_reference"] = {"runs": runs, "threads": threads, "tau_s": tau_c, "p": pref,
+                                "kind": kind,
                                 "tts99_s": tau_c * math.log(0.01) / math.log(1 - pref)}
     return out
+
+
+REF_STATS = os.path.join(REPO, "tests", "golden", "stats_large.npz")
+
+
+def binomial(k, n):
+    """k successes of n with the 95% Wilson score interval."""
+    import math
+    z = 1.96
+    ph = k / n
+    den = 1.0 + z * z / n
+    c = (ph + z * z / (2 * n)) / den
+    half = z * math.sqrt(ph * (1 - ph) / n + z * z / (4 * n * n)) / den
+    return {"k": int(k), "n": int(n), "p": ph, "ci95": [c - half, c + half]}
+
+
+def compare_p(k_gpu, n_gpu, k_ref, n_ref):
+    """North-star statistics criterion: the GPU's success probability inside the
+    reference's 95% binomial (Wilson) interval; the pooled two-proportion z is
+    reported beside it."""
+    import math
+    ref, gpu = binomial(k_ref, n_ref), binomial(k_gpu, n_gpu)
+    pool = (k_gpu + k_ref) / (n_gpu + n_ref)
+    se = math.sqrt(max(pool * (1 - pool), 1e-300) * (1 / n_gpu + 1 / n_ref))
+    return {"reference": ref, "gpu": gpu,
+            "gpu_p_in_reference_ci": ref["ci95"][0] <= gpu["p"] <= ref["ci95"][1],
+            "z": (gpu["p"] - ref["p"]) / se}
+
+
+def measure_statistics(nb, dev, workload, last_energies):
+    """Success probabilities against the reference's own large samples
+    (tests/golden/stats_large.npz, make_golden_stats.py: the reference's streams
+    and arithmetic, identical to nmfa_batch on every shared seed).
+
+    SK100 / Moebius-100: p(E <= ground) with the reference's best energy.
+    G2000 / K2000: p(E <= E*), E* = the reference sample's 10th-percentile
+    energy.  K2000 uses the timed steps' own last energies."""
+    import numpy as np
+
+    try:
+        ref = np.load(REF_STATS)
+    except OSError:
+        return None
+    out = {}
+    cases = [("sk100", "gen_sk(100, 0)", 65536, None), ("moebius100", "moebius_ladder(100)", 32768, None),
+             ("g2000", "gen_dense_maxcut(2000, 0.01, 7)", 4096, 0.1)]
+    for name, expr, reads, q in cases:
+        e_ref = ref[name + "_E"].astype(np.float64)
+        thr = e_ref.min() if q is None else float(np.quantile(e_ref, q, method="lower"))
+        p = eval("nb." + expr, {"nb": nb})
+        ev = (torch_event(), torch_event())
+        nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads, device=dev.index)   # warm the plan
+        ev[0].record()
+        res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads, device=dev.index)
+        ev[1].record()
+        ev[1].synchronize()
+        e = res.energies.cpu().numpy()
+        wall = ev[0].elapsed_time(ev[1]) * 1e-3
+        out[name] = {"threshold_E": thr, "threshold": "reference minimum" if q is None else
+                     "reference 10th percentile", "path": p.device_info(dev.index)["path"],
+                     "spin_updates_per_s": p.n * reads * 1000 / wall, "seed": 0,
+                     **compare_p(int(np.count_nonzero(e <= thr + 1e-9)), reads,
+                                 int(np.count_nonzero(e_ref <= thr + 1e-9)), e_ref.size)}
+    if workload == "k2000" and last_energies is not None:
+        e_ref = ref["sk2000_E"].astype(np.float64)
+        thr = float(np.quantile(e_ref, 0.1, method="lower"))
+        e = np.asarray(last_energies)
+        out["k2000"] = {"threshold_E": thr, "threshold": "reference 10th percentile",
+                        "note": "energies of the last timed step",
+                        **compare_p(int(np.count_nonzero(e <= thr + 1e-9)), e.size,
+                                    int(np.count_nonzero(e_ref <= thr + 1e-9)), e_ref.size)}
+    return out
+
+
+def torch_event():
+    import torch
+    return torch.cuda.Event(enable_timing=True)
 
 
 def run_reference(args):
@@ -325,8 +455,8 @@ def run_sk65536(args):
             "data": "synthetic (on-device Philox SK couplings)",
             "config": {"workload": desc, "reads_total": R, "n": n, "t_f": t_f,
                        "parallelism": f"J row-sharded x{world}", "setup_s": setup_s,
-                       "exchange": (f"{args.exchange}: " + ("epilogue peer stores into symmetric "
-                                    "memory + device barrier per sweep" if args.exchange == "p2p"
+                       "exchange": (f"{sk.exchange}: " + ("epilogue peer stores into symmetric "
+                                    "memory + device barrier per sweep" if sk.exchange == "p2p"
                                     else "NCCL all_gather_into_tensor per sweep")),
                        "l2": "J shard (8.6/G GB) exceeds L2; no flush needed",
                        "best_energy": best, "best_energy_per_spin": best / n},
@@ -448,8 +578,10 @@ def run_ours(args):
     lib = _native.load()
     stream = torch.cuda.current_stream(dev)
 
-    def step(k):
+    def step(k, mid=None):
         launches = plan.run(params.seed + 1000003 * k, r0, config=cfg, energy=en, stream=stream)
+        if mid is not None:
+            mid.record(stream)
         _native.check(lib.nmfa_best_of(_native.ptr(en), R, _native.ptr(best_e), _native.ptr(best_i),
                                        ctypes.c_void_p(stream.cuda_stream)))
         return launches + 1
@@ -463,19 +595,22 @@ def run_ours(args):
     # L2 is flushed between timed steps (a 256 MB write, outside the per-step
     # CUDA-event brackets), so no step starts with the previous step's J/state hot
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    # three events per step on the launching stream: start, after the anneal
+    # launch (the dominant kernel: all t_f sweeps + energies), after best-of
+    evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
             evs[k][0].record(stream)
-            launches += step(args.warmup + k)
-            evs[k][1].record(stream)
+            launches += step(args.warmup + k, mid=evs[k][1])
+            evs[k][2].record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    ms = sum(e0.elapsed_time(e2) for e0, _, e2 in evs)
+    anneal_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in evs) / args.steps
+    last_energies = en.double().cpu().numpy()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -491,16 +626,12 @@ def run_ours(args):
     gbest = allp[np.lexsort((allp[:, 1], allp[:, 0]))[0]]
     value = world * n * R * t_f * args.steps / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel: anneal-only launches, CUDA events on its stream
+    # ---- roofline of the dominant kernel, from the timed steps themselves: the
+    # anneal launch's CUDA-event time (same L2-flushed steps as `value`)
     info = p.device_info(local)
-    evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-    evs[0].record(stream)
-    n_anneal = plan.run(params.seed, r0, config=cfg, stream=stream)
-    evs[1].record(stream)
-    torch.cuda.synchronize(dev)
-    anneal_ms = evs[0].elapsed_time(evs[1])
     per_launch_s = anneal_ms * 1e-3 / t_f
     peaks, peak_src = load_peaks()
+    sm_mhz = clk.summary().get("sm_mhz")
     if info["path"] in ("dense", "small"):
         npad = (n + 15) // 16 * 16
         flop = 2.0 * n * n * R
@@ -508,9 +639,18 @@ def run_ours(args):
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
-                "kernel": f"{info['path']} NMFA step (tcgen05, fused epilogue)",
-                "algorithmic_per_launch": f"2*N^2*R = {flop:.4g} FLOP (N={n}, R={R}; padded N={npad})",
-                "avg_launch_us": per_launch_s * 1e6, "peak_source": f"{peak_src} bf16 sustained"}
+                "kernel": f"{info['path']} NMFA anneal (tcgen05, fused epilogue; one launch = t_f sweeps "
+                          "+ exact energies)",
+                "algorithmic_per_launch": f"2*N^2*R*t_f = {flop * t_f:.4g} FLOP (N={n}, R={R}, "
+                                          f"t_f={t_f}; padded N={npad}; energy pass not counted)",
+                "avg_launch_us": anneal_ms * 1e3, "avg_sweep_us": per_launch_s * 1e6,
+                "timing": "CUDA events around the anneal launch inside the timed, L2-flushed steps",
+                "peak_source": f"{peak_src} bf16 sustained (fp16 runs at the bf16 rate)",
+                "frac_of_burst": achieved / peaks.get("bf16_tflops", peak)}
+        if sm_mhz:
+            # tensor duty per clock: FLOP/clk/SM over the 8192 dense f16 FLOP/clk/SM
+            roof["per_clock_duty"] = achieved * 1e12 / (148 * sm_mhz * 1e6) / 8192
+            roof["per_clock_sm_mhz"] = sm_mhz
         if info["path"] == "small":
             roof["note"] = ("n <= 256 runs on chip for all t_f steps; the binding resource is the fused "
                             "update's instruction issue (ncu: 28 instructions per spin-update, IPC 2.1 "
@@ -522,6 +662,7 @@ def run_ours(args):
         peak = peaks.get("hbm_gbs")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
+                "timing": "CUDA events around the anneal launches inside the timed, L2-flushed steps",
                 "kernel": ("sparse NMFA step (ELL gather, %d slots per row, fused epilogue)" % info["ell_slots"]
                            if info.get("ell_slots") else "sparse NMFA step (CSR gather, fused epilogue)"),
                 "algorithmic_per_launch": f"R*N*8 + nnz*8 + (N+1)*4 = {byts:.4g} B",
@@ -569,6 +710,9 @@ def run_ours(args):
     tts = None
     if rank == 0 and not args.no_tts:
         tts = measure_tts_sk100(nb, dev, args.no_cpu_baseline)
+    stats = None
+    if rank == 0 and not args.no_stats:
+        stats = measure_statistics(nb, dev, args.workload, last_energies)
 
     cpu_bl = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -580,7 +724,7 @@ def run_ours(args):
             "metric": metric_name(args.workload), "value": value,
             "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16 operand / f32 state",
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[info["path"]],
             "data": f"synthetic (reference generator stream, {WORKLOADS[args.workload][0]})",
             "config": {"workload": desc, "reads_per_gpu": R, "reads_total": R * world,
                        "n": n, "t_f": t_f, "path": info["path"],
@@ -598,6 +742,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "tts99_sk100": tts,
+            "statistics": stats,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -617,8 +762,11 @@ def main():
     ap.add_argument("--ref-runs", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the SK100 TTS99 side measurement")
-    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
-                    help="sk65536: fused peer-store exchange (default) or NCCL all-gather")
+    ap.add_argument("--no-stats", action="store_true",
+                    help="skip the success-probability side measurements (SK100, Moebius-100, G2000)")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="nccl",
+                    help="sk65536: NCCL all-gather per sweep (default) or the fused peer-store "
+                         "exchange (p2p; falls back to NCCL when symmetric memory is unavailable)")
     args = ap.parse_args()
     if args.impl != "reference":
         # the CUDA library ships prebuilt with the snapshot; build it if it is

@@ -1267,7 +1267,10 @@ int dense_read_config(const nmfa_plan* pl, int8_t* cfg, cudaStream_t st) {
 }
 
 bool dense_energy_exact(const nmfa_problem* p) {
-  return p->int_weights && p->j_exact && p->max_row_abs / p->j_scale < 16777216.0;
+  // integer weights stored as J / j_scale lie on a 1/j_scale grid (j_scale a
+  // power of two); every fp32 partial row sum k / j_scale is exact while the
+  // integer |k| <= max_row_abs stays below 2^24
+  return p->int_weights && p->j_exact && p->max_row_abs < 16777216.0;
 }
 
 }  // namespace nmfa

@@ -26,6 +26,11 @@ static int arg_error(const std::string& msg) {
   return NMFA_ERR_ARG;
 }
 
+static int state_error(const std::string& msg) {
+  set_error(msg);
+  return NMFA_ERR_STATE;
+}
+
 template <class T>
 static int upload(T** dst, const T* src, size_t count) {
   if (count == 0) count = 1;  // keep a valid pointer for empty arrays
@@ -482,6 +487,12 @@ int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info) {
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
   NMFA_API_BEGIN
   if (!p) return arg_error("NULL problem");
+  if (path < 0 || path > 2) return arg_error("unknown path");
+  std::lock_guard<std::mutex> lock(p->cache_mu);
+  if (p->cached_plan) {  // a cached plan holds the old path's buffers
+    nmfa_plan_destroy(p->cached_plan);
+    p->cached_plan = nullptr;
+  }
   if (p->device_generated && path != NMFA_PATH_DENSE)
     return arg_error("a device-generated problem only runs the dense path");
   if (path == NMFA_PATH_SMALL && !p->d_j_small)
@@ -514,7 +525,6 @@ int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
       return err;
     }
   }
-  if (path < 0 || path > 2) return arg_error("unknown path");
   p->path = path;
   return NMFA_OK;
   NMFA_API_END
@@ -559,6 +569,7 @@ int nmfa_plan_create(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
   pl->p = p;
   pl->R = R;
   pl->t_f = t_f;
+  pl->path = p->path;
   pl->alpha = (float)alpha;
   pl->oma = (float)(1.0 - alpha);
   pl->sigma = (float)sigma;
@@ -609,6 +620,8 @@ int nmfa_plan_run(nmfa_plan_t* pl, uint64_t seed, int64_t r0, const float* noise
   if (e_hist && !s_hist) return arg_error("e_hist requires s_hist");
   g_launches = 0;
   const nmfa_problem* p = pl->p;
+  if (pl->path != p->path)
+    return state_error("plan was built for another path; create a new plan after set_path");
   cudaStream_t st = (cudaStream_t)stream;
   int prev = 0;
   cudaGetDevice(&prev);

@@ -19,19 +19,23 @@ namespace nmfa {
 // bits[i * W + wd] bit l  <=>  cfg[(32*wd + l) * n + i] < 0
 __global__ void pack_bits_kernel(const int8_t* __restrict__ cfg, long long R, int n, long long W,
                                  uint32_t* __restrict__ bits) {
+  // word index on grid.x (R * t_f configurations can exceed 65535 * 32), 128-spin
+  // blocks on grid.y, strided when n / 128 exceeds the grid
   __shared__ int8_t tile[32][129];
-  const long long wd = blockIdx.y;
-  const int i0 = blockIdx.x * 128;
-  for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
-    const int rr = e >> 7, ii = e & 127;
-    const long long r = wd * 32 + rr;
-    tile[rr][ii] = (r < R && i0 + ii < n) ? cfg[r * n + i0 + ii] : (int8_t)1;
-  }
-  __syncthreads();
+  const long long wd = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int ii = warp; ii < 128; ii += blockDim.x >> 5) {
-    const uint32_t b = __ballot_sync(0xffffffffu, tile[lane][ii] < 0);
-    if (lane == 0 && i0 + ii < n) bits[(long long)(i0 + ii) * W + wd] = b;
+  for (long long i0 = (long long)blockIdx.y * 128; i0 < n; i0 += (long long)gridDim.y * 128) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
+      const int rr = e >> 7, ii = e & 127;
+      const long long r = wd * 32 + rr;
+      tile[rr][ii] = (r < R && i0 + ii < n) ? cfg[r * n + i0 + ii] : (int8_t)1;
+    }
+    __syncthreads();
+    for (int ii = warp; ii < 128; ii += blockDim.x >> 5) {
+      const uint32_t b = __ballot_sync(0xffffffffu, tile[lane][ii] < 0);
+      if (lane == 0 && i0 + ii < n) bits[(i0 + ii) * W + wd] = b;
+    }
   }
 }
 
@@ -107,7 +111,7 @@ int64_t energy_chunks_for(const nmfa_problem* p, int64_t n_cfg) {
 int launch_energy(const nmfa_problem* p, const int8_t* cfg, int64_t R, double* energy,
                   uint32_t* bits, double* part, int64_t chunks, cudaStream_t st) {
   const long long W = (R + 31) / 32;
-  dim3 g1((unsigned)((p->n + 127) / 128), (unsigned)W);
+  dim3 g1((unsigned)W, (unsigned)std::min<long long>((p->n + 127) / 128, 65535));
   pack_bits_kernel<<<g1, 256, 0, st>>>(cfg, R, (int)p->n, W, bits);
   NMFA_LAUNCH_CHECK();
   // `part` holds chunks + 1 rows (energy_chunks_for): field rows first claimed

@@ -193,6 +193,7 @@ int gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out, in
     return fail(ps.line_no, "non-numeric header token in " + py_list_repr(t));
   if (n < 1) return fail(ps.line_no, "vertex count must be positive, got " + std::to_string(n));
   if (m < 0) return fail(ps.line_no, "edge count must be nonnegative, got " + std::to_string(m));
+  if (n > (1LL << 30)) return fail(ps.line_no, "vertex count too large, got " + std::to_string(n));
   *n_out = n;
   *m_out = m;
   if (!ei) return NMFA_OK;  // header query
@@ -204,7 +205,8 @@ int gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out, in
   // the earliest failure (parse error or duplicate) wins
   // duplicates: an n x n bitset checked in file order when it is small
   // (<= 64 MB, n <~ 23k), else one sort after the pass
-  const bool use_bits = (unsigned long long)n * (unsigned long long)n <= (64ULL << 23);
+  // (n <= 23170 keeps n * n far from 64-bit overflow; larger n sorts)
+  const bool use_bits = n <= 23170 && (unsigned long long)n * (unsigned long long)n <= (64ULL << 23);
   std::vector<uint64_t> seen(use_bits ? ((unsigned long long)n * n + 63) / 64 : 0, 0);
   std::vector<long long> line_of;
   line_of.reserve((size_t)std::min<long long>(m, (long long)len / 4 + 1));  // m may be absurd

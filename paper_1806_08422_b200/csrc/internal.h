@@ -94,6 +94,7 @@ struct nmfa_plan {
   const nmfa_problem* p = nullptr;
   int64_t R = 0;
   int32_t t_f = 0;
+  int32_t path = 0;             // the problem's path when the plan was built
   float alpha = 0.f, oma = 0.f, sigma = 0.f;
   float* d_inv_temp = nullptr;  // [t_f]
   std::vector<float> h_inv_temp; // host copy (per-step launches read it)

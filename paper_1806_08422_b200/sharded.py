@@ -99,6 +99,43 @@ def allreduce_sum(t, group=None):
     return t
 
 
+class ShardProtocol:
+    """The per-anneal host protocol of a row-sharded plan, independent of where
+    the shard computes (CUDA plan here; a CPU stand-in in tests/test_sharded.py).
+
+    A shard provides: world, rank, R, params, images[2] (flat uint8 tensors),
+    slice_lo/slice_hi/slice_bytes, group, sweeps(seed, t_begin, t_end, r0,
+    energy, stream), new_energy(), read_config(stream), exchange_after(t,
+    stream)."""
+
+    def exchange_after(self, t, stream=None):
+        """Make sweep t's new image (parity (t + 1) & 1) complete on every shard."""
+        exchange_slices(self.images[(t + 1) & 1], self.slice_lo, self.slice_hi, self.slice_bytes,
+                        self.group)
+
+    def run(self, seed, r0=0, stream=None):
+        """One anneal of all t_f sweeps; returns configs and exact total energies.
+
+        G = 1: one persistent launch (all sweeps + the energy pass).  G > 1: per
+        sweep t one launch on the shard, then the exchange of image (t+1) & 1;
+        after the last sweep the energy pass gives per-shard partials of
+        1/2 sum_i c_i (J c)_i + h.c (integers in f64), summed over the ranks."""
+        t_f = self.params.t_f
+        en = self.new_energy()
+        if self.world == 1:
+            self.sweeps(seed, 0, t_f, r0, energy=en, stream=stream)
+        else:
+            for t in range(t_f):
+                self.sweeps(seed, t, t + 1, r0, stream=stream)
+                self.exchange_after(t, stream)
+            self.sweeps(seed, t_f, t_f, r0, energy=en, stream=stream)
+            self.reduce_energy(en, stream)
+        return ShardedResult(self.read_config(stream), en, t_f)
+
+    def reduce_energy(self, en, stream=None):
+        allreduce_sum(en, self.group)
+
+
 @dataclass
 class ShardedResult:
     configs: object        # torch.int8 (R, n) on this rank's device (all spins)
@@ -106,7 +143,7 @@ class ShardedResult:
     sweeps: int
 
 
-class RowShardedSK:
+class RowShardedSK(ShardProtocol):
     """Synthetic SK instance with J row-sharded over the ranks of `group`."""
 
     def __init__(self, n, seed, n_reads, params=None, group=None, device=None, shard=None,
@@ -153,7 +190,12 @@ class RowShardedSK:
         self.exchange = exchange
         self._symm = None
         if exchange == "p2p" and self.world > 1 and shard is None:
-            self._setup_p2p(nbytes, dev)
+            try:
+                self._setup_p2p(nbytes, dev)
+            except Exception as exc:  # no symmetric memory / multicast here: NCCL exchange
+                import warnings
+                warnings.warn(f"fused p2p exchange unavailable ({exc}); using the NCCL all-gather")
+                self.exchange = "nccl"
 
     def _setup_p2p(self, nbytes, dev):
         """Symmetric-memory images + pointer exchange (nmfa_plan_set_exchange)."""
@@ -195,28 +237,22 @@ class RowShardedSK:
         _native.check(_native.load().nmfa_plan_read_config(self.plan, _native.ptr(cfg), sp))
         return cfg
 
-    def run(self, seed, r0=0, stream=None):
-        """One anneal of all t_f sweeps; returns configs and exact total energies."""
+    def new_energy(self):
         import torch
+        return torch.empty(self.R, dtype=torch.float64, device=torch.device("cuda", self.device))
 
-        stream = self._stream(stream)
-        t_f = self.params.t_f
-        en = torch.empty(self.R, dtype=torch.float64, device=torch.device("cuda", self.device))
-        if self.world == 1:
-            self.sweeps(seed, 0, t_f, r0, energy=en, stream=stream)
-        else:
-            for t in range(t_f):
-                self.sweeps(seed, t, t + 1, r0, stream=stream)
-                with torch.cuda.stream(stream):
-                    if self._symm is not None:
-                        self._barrier()
-                    else:
-                        exchange_slices(self.images[(t + 1) & 1], self.slice_lo, self.slice_hi,
-                                        self.slice_bytes, self.group)
-            self.sweeps(seed, t_f, t_f, r0, energy=en, stream=stream)
-            with torch.cuda.stream(stream):
-                allreduce_sum(en, self.group)
-        return ShardedResult(self.read_config(stream), en, t_f)
+    def exchange_after(self, t, stream=None):
+        import torch
+        with torch.cuda.stream(self._stream(stream)):
+            if self._symm is not None:
+                self._barrier()          # the epilogue already stored into every image
+            else:
+                super().exchange_after(t, stream)
+
+    def reduce_energy(self, en, stream=None):
+        import torch
+        with torch.cuda.stream(self._stream(stream)):
+            allreduce_sum(en, self.group)
 
     def __del__(self):
         try:

@@ -221,42 +221,6 @@ def test_best_of_matches_numpy():
     assert be == arr.min() and bi == int(np.argmin(arr))
 
 
-def _two_sample_z(k1, n1, k2, n2):
-    p = (k1 + k2) / (n1 + n2)
-    se = np.sqrt(p * (1 - p) * (1 / n1 + 1 / n2))
-    return abs(k1 / n1 - k2 / n2) / se if se > 0 else 0.0
-
-
-def test_success_probability_sk100_consistent_with_reference(G):
-    S = G["stats"]
-    ref = S["sk100_E"]
-    k_ref = int(np.count_nonzero(ref <= -730 + 1e-9))
-    p = nb.gen_sk(100, 0)
-    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 16384)
-    e = res.energies.cpu().numpy()
-    assert e.min() >= -730.0
-    k = int(np.count_nonzero(e <= -730 + 1e-9))
-    z = _two_sample_z(k, e.size, k_ref, ref.size)
-    lo, hi = nb.wilson_interval(k_ref, ref.size)
-    print(f"sk100 p_gpu={k / e.size:.4f} p_ref={k_ref / ref.size:.4f} ref CI=({lo:.4f},{hi:.4f}) z={z:.2f}")
-    assert z < 4.0
-
-
-@pytest.mark.parametrize("path", ["small", "sparse"])
-def test_success_probability_moebius100_consistent_with_reference(G, path):
-    ref = G["stats"]["moebius100_E"]
-    k_ref = int(np.count_nonzero(ref <= -146 + 1e-9))
-    p = nb.moebius_ladder(100)
-    p.device_handle().set_path(path)
-    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 8192)
-    e = res.energies.cpu().numpy()
-    assert e.min() >= -146.0
-    k = int(np.count_nonzero(e <= -146 + 1e-9))
-    z = _two_sample_z(k, e.size, k_ref, ref.size)
-    print(f"moebius100[{path}] p_gpu={k / e.size:.4f} p_ref={k_ref / ref.size:.4f} z={z:.2f}")
-    assert z < 4.0
-
-
 def test_moebius16_reaches_ground(G):
     p = nb.moebius_ladder(16)
     res = nb.nmfa_batch(p, nb.NmfaParams(t_f=100, seed=0), 100)
@@ -265,29 +229,6 @@ def test_moebius16_reaches_ground(G):
     traj = nb.nmfa_run(p, nb.NmfaParams(t_f=100, seed=0), record_trajectory=True).trajectory
     mag = np.abs(traj.spins).mean(axis=1)
     assert mag[0] < 0.2 and mag[-1] > 0.8 and mag[-1] > mag[50] > mag[0]
-
-
-@pytest.mark.parametrize("path", ["auto", "sparse"])
-def test_g2000_energy_distribution(G, path):
-    ref = G["stats"]["g2000_E"]
-    p = nb.gen_dense_maxcut(2000, 0.01, 7)
-    # 1% density at n=2000: the tensor-core path is faster than the CSR gather
-    assert p.device_info()["path"] == "dense"
-    if path == "sparse":
-        p.device_handle().set_path("sparse")
-    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 1024)
-    e = res.energies.cpu().numpy()
-    se = np.sqrt(ref.var(ddof=1) / ref.size + e.var(ddof=1) / e.size)
-    print(f"g2000[{path}] mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
-          f"min_ref={ref.min()} se={se:.2f}")
-    assert abs(e.mean() - ref.mean()) < 4 * se
-    # SURVEY 8(d) C4 success criterion: E <= E*, the reference's 10th-percentile energy
-    e_star = np.quantile(ref, 0.1)
-    p_ref, p_gpu = np.mean(ref <= e_star), np.mean(e <= e_star)
-    pool = (p_ref * ref.size + p_gpu * e.size) / (ref.size + e.size)
-    z = (p_gpu - p_ref) / np.sqrt(pool * (1 - pool) * (1 / ref.size + 1 / e.size))
-    print(f"g2000[{path}] E*={e_star} p_ref={p_ref:.3f} p_gpu={p_gpu:.3f} z={z:.2f}")
-    assert abs(z) < 3.5
 
 
 def test_host_entry_point_matches_device_api():
@@ -324,21 +265,6 @@ def test_dense_large_injected_noise_matches_oracle():
           f"sign flips={flips:.2e}")
     assert np.mean(err) < 1e-3 and np.mean(err > 2e-2) < 5e-3, (np.mean(err), err.max())
     assert flips <= 1e-3, flips
-
-
-def test_k2000_standin_energy_distribution(G):
-    ref = G["stats"]["sk2000_E"]
-    p = nb.gen_sk(2000, 7)
-    assert p.device_info()["path"] == "dense"
-    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), 1024)
-    e = res.energies.cpu().numpy()
-    op = O.problem_from_edges(2000, p.edges_i, p.edges_j, p.edge_weights)
-    cfg = res.configs[:64].cpu().numpy().astype(np.float64)
-    assert np.array_equal(e[:64], O.energies(op, cfg))
-    se = np.sqrt(ref.var(ddof=1) / ref.size + e.var(ddof=1) / e.size)
-    print(f"k2000 mean_gpu={e.mean():.1f} mean_ref={ref.mean():.1f} min_gpu={e.min()} "
-          f"min_ref={ref.min()} se={se:.2f}")
-    assert abs(e.mean() - ref.mean()) < 4 * se
 
 
 def test_host_entry_is_thread_safe():

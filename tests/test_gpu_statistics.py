@@ -1,0 +1,78 @@
+"""Seeded success statistics against the reference (north star, correctness
+leg 3): "ground-state success probability per instance falls within the
+reference's binomial confidence interval".
+
+Reference samples: tests/golden/stats_large.npz (make_golden_stats.py) --
+SK100 65,536 reads, Moebius-100 32,768, G2000 and the K2000 stand-in 4,096
+each, produced from the reference's own per-run noise streams and arithmetic
+and identical to `nmfa_batch` on every seed the two share.
+
+Criterion, per instance and path: the GPU's p lies inside the reference's
+95% Wilson interval (metrics.py:70-75 defines p).  Success is E <= the
+reference's minimum (SK100, Moebius-100: the best-known energies -730 and
+-146) or E <= E*, the reference sample's 10th-percentile energy (G2000,
+K2000: SURVEY 8(d) C4).  The GPU sample is 2-4x the reference's so the
+interval is set by the reference's own sampling error.  The GPU's seeded
+noise is its own counter-based stream, so agreement is
+statistical, not per seed.
+"""
+
+import numpy as np
+import pytest
+
+import nmfa_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1806_08422_b200 as nb  # noqa: E402
+from paper_1806_08422_b200 import _native  # noqa: E402
+
+from conftest import golden  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1806_08422_b200 import build
+    build.build()
+    _native.load()
+
+
+REF = golden("stats_large.npz")
+
+CASES = {  # name: (builder, GPU reads, threshold rule, paths)
+    "sk100": (lambda: nb.gen_sk(100, 0), 131072, "min", ["small"]),
+    "moebius100": (lambda: nb.moebius_ladder(100), 65536, "min", ["small", "sparse"]),
+    "g2000": (lambda: nb.gen_dense_maxcut(2000, 0.01, 7), 8192, "q10", ["dense", "sparse"]),
+    "sk2000": (lambda: nb.gen_sk(2000, 7), 8192, "q10", ["dense"]),
+}
+
+
+def threshold(e_ref, rule):
+    return float(e_ref.min()) if rule == "min" else float(np.quantile(e_ref, 0.1, method="lower"))
+
+
+@pytest.mark.parametrize("name,path", [(k, p) for k, v in CASES.items() for p in v[3]])
+def test_success_probability_inside_reference_ci(name, path):
+    make, reads, rule, _ = CASES[name]
+    e_ref = REF[name + "_E"].astype(np.float64)
+    thr = threshold(e_ref, rule)
+    k_ref = int(np.count_nonzero(e_ref <= thr + 1e-9))
+    lo, hi = O.wilson_interval(k_ref, e_ref.size)
+    p = make()
+    p.device_handle().set_path(path)
+    res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads)
+    e = res.energies.cpu().numpy()
+    k = int(np.count_nonzero(e <= thr + 1e-9))
+    pg = k / e.size
+    pool = (k + k_ref) / (e.size + e_ref.size)
+    z = (pg - k_ref / e_ref.size) / np.sqrt(pool * (1 - pool) * (1 / e.size + 1 / e_ref.size))
+    print(f"{name}[{path}] E_thr={thr:.0f} p_gpu={pg:.4f} ({k}/{e.size}) p_ref={k_ref / e_ref.size:.4f} "
+          f"ref 95% CI=[{lo:.4f}, {hi:.4f}] z={z:+.2f} mean E gpu={e.mean():.2f} ref={e_ref.mean():.2f}")
+    if rule == "min":   # nothing below the best-known energy
+        assert e.min() >= thr - 1e-9
+    assert lo <= pg <= hi, (pg, lo, hi)
+

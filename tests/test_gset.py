@@ -62,3 +62,21 @@ def test_large_instance_parses_fast():
     dt = time.perf_counter() - t
     assert q.num_edges == p.num_edges and np.array_equal(q.edge_weights, p.edge_weights)
     assert dt < 3.0, dt
+
+
+@pytest.mark.parametrize("n", [4294967296, 3037000500, (1 << 30) + 1])
+def test_absurd_vertex_count_is_rejected_not_overflowed(n):
+    """A header whose n * n wraps 64 bits must not size the duplicate bitset
+    from the wrapped product (n = 2^32 used to segfault)."""
+    with pytest.raises(nb.GsetParseError) as exc:
+        nb.parse_gset(f"{n} 2\n1 2 1\n2 3 1\n")
+    assert exc.value.line_no == 1 and "vertex count too large" in str(exc.value)
+
+
+def test_large_n_without_bitset_still_finds_duplicates():
+    """n above the bitset limit (23170) takes the sort path for duplicates."""
+    with pytest.raises(nb.GsetParseError) as exc:
+        nb.parse_gset("100000 3\n1 2 1\n5 9 1\n2 1 1\n")
+    assert exc.value.line_no == 4 and "duplicate edge (1, 2)" in str(exc.value)
+    p = nb.parse_gset("100000 2\n1 2 1\n99999 100000 -1\n")
+    assert p.n == 100000 and p.edges_j.tolist() == [1, 99999]

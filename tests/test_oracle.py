@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import nmfa_oracle as O
+from conftest import golden
 
 
 def sha(a):
@@ -146,3 +147,16 @@ def test_tts_and_stats_kats(G):
     assert p == pytest.approx(0.2334, abs=1e-4)
     lo, hi = O.wilson_interval(int(round(p * 10000)), 10000)
     assert lo < p < hi and hi - lo < 0.02
+
+
+def test_large_reference_samples_are_pinned_to_nmfa_batch():
+    """stats_large.npz (make_golden_stats.py: the reference's streams and
+    arithmetic, replica-batched) agrees with the reference's own nmfa_batch
+    energies (stats.npz) on every seed the two share."""
+    big, small = golden("stats_large.npz"), golden("stats.npz")
+    sizes = {"sk100": 65536, "moebius100": 32768, "g2000": 4096, "sk2000": 4096}
+    for name, size in sizes.items():
+        same, m = big[name + "_same_as_nmfa_batch"]
+        assert same == m and m >= 64, name
+        assert big[name + "_E"].size == size and int(big[name + "_t_f"]) == 1000
+        assert np.array_equal(big[name + "_E"][:m].astype(np.float64), small[name + "_E"][:m])

@@ -92,3 +92,93 @@ def test_device_normals_spec_moments():
     assert np.abs(z).max() <= np.sqrt(-2 * np.log(0.5 * 2.0 ** -20)) + 1e-12
     z1 = O.device_normals(7, np.arange(0, 4), 1, 64, 1.0)
     assert not np.allclose(z[:4], z1) and not np.allclose(z[0], z[1])
+
+
+# ---------------------------------------------------------------------------
+# The full RowShardedSK.run host protocol (ShardProtocol.run) under gloo world 2,
+# with a CPU stand-in for the CUDA shard: same image geometry (k-slice-major
+# flat bytes, one contiguous chunk per rank), same sweep / exchange / energy
+# pass / all-reduce order.  Compared with the unsharded (world 1) run.
+# ---------------------------------------------------------------------------
+from paper_1806_08422_b200.sharded import ShardProtocol  # noqa: E402
+from paper_1806_08422_b200.solver import NmfaParams  # noqa: E402
+
+
+class CpuShard(ShardProtocol):
+    SLICE = 128
+
+    def __init__(self, J, R, params, world, rank, group=None):
+        self.J, self.n, self.R, self.params = J, J.shape[0], R, params
+        self.world, self.rank, self.group = world, rank, group
+        self.n_slices = self.n // self.SLICE
+        per = self.n_slices // world
+        self.slice_lo, self.slice_hi = rank * per, (rank + 1) * per
+        self.slice_bytes = R * self.SLICE * 8                  # float64 state, [slice][r][128]
+        self.images = [torch.zeros(self.n_slices * self.slice_bytes, dtype=torch.uint8)
+                       for _ in range(2)]
+        self.norm = np.sqrt((J ** 2).sum(axis=1))
+        self.temps = params.schedule.temperatures(params.t_f)
+
+    def state(self, parity):
+        v = self.images[parity].numpy().view(np.float64).reshape(self.n_slices, self.R, self.SLICE)
+        return v.transpose(1, 0, 2).reshape(self.R, self.n)       # (R, n) copy
+
+    def noise(self, seed, r0, t):
+        # keyed by (global replica, step): the same values whatever the sharding
+        return np.stack([np.random.default_rng([seed, r0 + r, t]).standard_normal(self.n)
+                         for r in range(self.R)]) * self.params.sigma
+
+    def sweeps(self, seed, t_begin, t_end, r0=0, energy=None, stream=None):
+        a, lo, hi = self.params.alpha, self.slice_lo * self.SLICE, self.slice_hi * self.SLICE
+        for t in range(t_begin, t_end):
+            S = self.state(t & 1)
+            phi = S @ self.J[lo:hi].T / self.norm[lo:hi] + self.noise(seed, r0, t)[:, lo:hi]
+            new = a * -np.tanh(phi / self.temps[t]) + (1 - a) * S[:, lo:hi]
+            if t == self.params.t_f - 1:
+                new = np.where(new < 0, -1.0, 1.0)      # the last sweep writes the +-1 config
+            dst = self.images[(t + 1) & 1].numpy().view(np.float64).reshape(
+                self.n_slices, self.R, self.SLICE)
+            dst[self.slice_lo:self.slice_hi] = new.reshape(self.R, -1, self.SLICE).transpose(1, 0, 2)
+        if energy is not None:
+            c = self.state(self.params.t_f & 1)
+            part = 0.5 * np.einsum("ri,ri->r", c[:, lo:hi], c @ self.J[lo:hi].T)
+            energy.copy_(torch.from_numpy(part))
+
+    def new_energy(self):
+        return torch.zeros(self.R, dtype=torch.float64)
+
+    def read_config(self, stream=None):
+        return torch.from_numpy(self.state(self.params.t_f & 1).astype(np.int8))
+
+
+def _protocol_J(n=256):
+    J = O.sk_device_couplings(n, 3)
+    return J
+
+
+def _protocol_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shard = CpuShard(_protocol_J(), 8, NmfaParams(t_f=40, seed=5), world, rank)
+        res = shard.run(5, r0=16)
+        out[rank] = (res.configs.numpy().copy(), res.energies.numpy().copy(), res.sweeps)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_protocol_world2_equals_unsharded():
+    J = _protocol_J()
+    solo = CpuShard(J, 8, NmfaParams(t_f=40, seed=5), 1, 0).run(5, r0=16)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_protocol_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    want_e = 0.5 * np.einsum("ri,ri->r", solo.configs.numpy().astype(np.float64),
+                             solo.configs.numpy().astype(np.float64) @ J)
+    assert np.allclose(solo.energies.numpy(), want_e)
+    for g in range(2):
+        cfg, en, sweeps = out[g]
+        assert sweeps == 40
+        assert np.array_equal(cfg, solo.configs.numpy()), g      # every rank sees all spins
+        assert np.array_equal(en, solo.energies.numpy()), g      # integers: exact all-reduce
