@@ -315,8 +315,10 @@ def measure_statistics(nb, dev, workload, last_energies):
     and arithmetic, identical to nmfa_batch on every shared seed).
 
     SK100 / Moebius-100: p(E <= ground) with the reference's best energy.
-    G2000 / K2000: p(E <= E*), E* = the reference sample's 10th-percentile
-    energy.  K2000 uses the timed steps' own last energies."""
+    G2000 / K2000: p(E <= E*), E* = the 10th-percentile energy of the first
+    4096 reference reads, the reference's p scored on the
+    reads after those (tests/test_gpu_statistics.py explains why).  K2000 uses
+    the timed steps' own last energies."""
     import numpy as np
 
     try:
@@ -325,10 +327,15 @@ def measure_statistics(nb, dev, workload, last_energies):
         return None
     out = {}
     cases = [("sk100", "gen_sk(100, 0)", 65536, None), ("moebius100", "moebius_ladder(100)", 32768, None),
-             ("g2000", "gen_dense_maxcut(2000, 0.01, 7)", 4096, 0.1)]
+             ("g2000", "gen_dense_maxcut(2000, 0.01, 7)", 16384, 0.1)]
+    def reference_success(e_ref, q):
+        if q is None:
+            return float(e_ref.min()), e_ref
+        thr = float(np.quantile(e_ref[:4096], q, method="lower"))
+        return thr, (e_ref[4096:] if e_ref.size > 4096 else e_ref)
+
     for name, expr, reads, q in cases:
-        e_ref = ref[name + "_E"].astype(np.float64)
-        thr = e_ref.min() if q is None else float(np.quantile(e_ref, q, method="lower"))
+        thr, e_ref = reference_success(ref[name + "_E"].astype(np.float64), q)
         p = eval("nb." + expr, {"nb": nb})
         ev = (torch_event(), torch_event())
         nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads, device=dev.index)   # warm the plan
@@ -339,15 +346,14 @@ def measure_statistics(nb, dev, workload, last_energies):
         e = res.energies.cpu().numpy()
         wall = ev[0].elapsed_time(ev[1]) * 1e-3
         out[name] = {"threshold_E": thr, "threshold": "reference minimum" if q is None else
-                     "reference 10th percentile", "path": p.device_info(dev.index)["path"],
+                     "10th percentile of the first 4096 reference reads; reference p over the rest", "path": p.device_info(dev.index)["path"],
                      "spin_updates_per_s": p.n * reads * 1000 / wall, "seed": 0,
                      **compare_p(int(np.count_nonzero(e <= thr + 1e-9)), reads,
                                  int(np.count_nonzero(e_ref <= thr + 1e-9)), e_ref.size)}
     if workload == "k2000" and last_energies is not None:
-        e_ref = ref["sk2000_E"].astype(np.float64)
-        thr = float(np.quantile(e_ref, 0.1, method="lower"))
+        thr, e_ref = reference_success(ref["sk2000_E"].astype(np.float64), 0.1)
         e = np.asarray(last_energies)
-        out["k2000"] = {"threshold_E": thr, "threshold": "reference 10th percentile",
+        out["k2000"] = {"threshold_E": thr, "threshold": "10th percentile of the first 4096 reference reads; reference p over the rest",
                         "note": "energies of the last timed step",
                         **compare_p(int(np.count_nonzero(e <= thr + 1e-9)), e.size,
                                     int(np.count_nonzero(e_ref <= thr + 1e-9)), e_ref.size)}

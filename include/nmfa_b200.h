@@ -219,6 +219,13 @@ const char* nmfa_version(void);
 /* Number of kernels the last nmfa_plan_run on this thread enqueued. */
 int64_t nmfa_last_launch_count(void);
 
+/* Checked build only (libnmfa_b200_guard.so, -DNMFA_GUARD; the memcheck
+ * substitute where compute-sanitizer is unavailable): synchronises the device
+ * and returns the number of redzone bytes found corrupted around the
+ * library's own device allocations (live ones now, freed ones when they were
+ * freed); nmfa_last_error() names the first.  Returns -1 in normal builds. */
+int64_t nmfa_debug_guard_check(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,10 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnmfa_b200.so")
+# NMFA_LIB=guard selects the checked build (redzones + protocol jitter,
+# csrc/guard.cu) for the guard tests; the default is the product library.
+LIB_PATH = os.path.join(_HERE, "libnmfa_b200_guard.so" if os.environ.get("NMFA_LIB") == "guard"
+                        else "libnmfa_b200.so")
 
 NMFA_OK, NMFA_ERR_ARG, NMFA_ERR_CUDA, NMFA_ERR_STATE = 0, 1, 2, 3
 PATH_SMALL, PATH_DENSE, PATH_SPARSE = 0, 1, 2
@@ -40,6 +43,7 @@ SIGNATURES = {
     "nmfa_last_error": (ctypes.c_char_p, []),
     "nmfa_version": (ctypes.c_char_p, []),
     "nmfa_last_launch_count": (_i64, []),
+    "nmfa_debug_guard_check": (_i64, []),
     "nmfa_problem_create_sk_device": (_i32, [_i64, _u64, _i64, _i64, _i32, ctypes.POINTER(_p)]),
     "nmfa_plan_run_sweeps": (_i32, [_p, _u64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "nmfa_plan_image_info": (_i32, [_p, ctypes.POINTER(_p), ctypes.POINTER(_p),

@@ -379,6 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             if (t2 && ki == 0) t2[5] = gtimer();
             if (t2 && ki == a.kblocks - 1) t2[1] = gtimer();
             const int s = it % kDStages;
+            NMFA_JITTER(blockIdx.x, it);  // checked build only
             if (a.trace) {
               const long long c0 = clock64();
               mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
@@ -427,6 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           long long wfull = 0;
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
             const int s = it % kDStages;
+            NMFA_JITTER(blockIdx.x + 7919, it);  // checked build only
             if (a.trace) {
               const long long c0 = clock64();
               mbar_wait(&full_bar[s], (it / kDStages) & 1);
@@ -640,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           for (; c + 16 <= c_hi; c += 16) do_chunk(std::integral_constant<int, 16>{}, c);
           if (c < c_hi) do_chunk(std::integral_constant<int, 8>{}, c);
         }
+        NMFA_JITTER(threadIdx.x + 641 * blockIdx.x, jj);  // checked build only
         tc_fence_before();
         __syncwarp();
         if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 512) atomicMax(&a.trace[jj * 8 + 5], clock64());
@@ -921,7 +924,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   const bool early = korder_env && std::string(korder_env) == "early";
   // debug knob NMFA_KORDER=rotate: tile j starts at its own spin range's k-slice
   // (spreads the concurrent reads of tiles that share A/J lines; timing only)
-  const bool rotate = korder_env && std::string(korder_env) == "rotate";
+  // rotm: by the replica block (pairs sharing a J tile start apart); rotmn: by both
+  const std::string kord_s = korder_env ? korder_env : "";
+  const bool rotate = kord_s == "rotate" || kord_s == "rotm" || kord_s == "rotmn";
   std::vector<int> avail((size_t)mb * kbn, 0);
   for (int q = 0; q < pairs; ++q)
     for (int j = off[q]; j < off[q + 1]; ++j) {
@@ -936,7 +941,8 @@ int dense_plan_alloc(nmfa_plan* pl) {
     t.pad = kbn - 1;  // position of the short last k-slice in the tile's K order
     if (rotate) {
       int16_t* ko = &korder[(size_t)j * kbn];
-      const int s0 = ((t.n0 - (int)p->row_lo) >> 7) % kbn;
+      const int sn = (t.n0 - (int)p->row_lo) >> 7;
+      const int s0 = (kord_s == "rotm" ? 3 * t.m_blk : kord_s == "rotmn" ? sn + 3 * t.m_blk : sn) % kbn;
       for (int k = 0; k < kbn; ++k) ko[k] = (int16_t)((k + s0) % kbn);
       t.pad = (kbn - 1 - s0 + kbn) % kbn;
       continue;

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
         }
       }
     }
+    NMFA_JITTER(threadIdx.x + 977 * blockIdx.x, t);  // checked build only
     tmem_wait_st();
     fence_proxy_async_smem();
     tc_fence_before();

@@ -191,6 +191,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Checked build (NMFA_GUARD, guard.cu): a pseudo-random sleep at protocol
+// points of the persistent kernels, so an ordering bug shows up as a result
+// that differs from the unchecked library.  Nothing in normal builds.
+#ifdef NMFA_GUARD
+#define NMFA_JITTER(a, b)                                                              \
+  do {                                                                                 \
+    unsigned _h = (unsigned)(a) * 0x9E3779B9u ^ (unsigned)(b) * 0x85EBCA6Bu ^ (unsigned)clock(); \
+    _h ^= _h >> 15;                                                                    \
+    _h *= 0x2C1B3C6Du;                                                                 \
+    if ((_h >> 28) < 3) __nanosleep((_h >> 8) & 4095);                                 \
+  } while (0)
+#else
+#define NMFA_JITTER(a, b) \
+  do {                    \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)

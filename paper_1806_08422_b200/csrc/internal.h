@@ -154,3 +154,19 @@ int launch_sign(const float* s, int64_t count, int8_t* cfg, cudaStream_t st);
 int launch_best_of(const double* e, int64_t n, double* best_e, int64_t* best_i,
                    cudaStream_t st);
 }  // namespace nmfa
+
+#ifdef NMFA_GUARD
+// Checked build: every device allocation goes through the redzone allocator
+// (guard.cu).  Defined last, after the CUDA runtime declarations, so only the
+// library's own call sites are redirected.
+namespace nmfa {
+cudaError_t guard_malloc(void** p, size_t n);
+cudaError_t guard_free(void* p);
+cudaError_t guard_malloc_async(void** p, size_t n, cudaStream_t st);
+cudaError_t guard_free_async(void* p, cudaStream_t st);
+}  // namespace nmfa
+#define cudaMalloc(p, n) ::nmfa::guard_malloc(reinterpret_cast<void**>(p), (size_t)(n))
+#define cudaFree(p) ::nmfa::guard_free((void*)(p))
+#define cudaMallocAsync(p, n, st) ::nmfa::guard_malloc_async(reinterpret_cast<void**>(p), (size_t)(n), (st))
+#define cudaFreeAsync(p, st) ::nmfa::guard_free_async((void*)(p), (st))
+#endif

@@ -67,6 +67,9 @@ def _chunk(args):
         z = noise_stream(r0 + k).standard_normal((t_f, n))
         z *= SIGMA
         noise[:, :, k] = z
+    if name == "g2000":  # 1% density: CSR product, same per-row sums up to order (ulp-level)
+        import scipy.sparse as sp
+        J = sp.csr_matrix(J)
     h = p.h[:, None]
     norm = p.normalizers_safe[:, None]
     S = np.zeros((n, R))
@@ -91,6 +94,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--extend", type=int, default=0,
+                    help="grow the --only samples to this many reads (appends seeds past the stored ones)")
     a = ap.parse_args()
     workers = os.cpu_count() or 8
     ref = np.load(os.path.join(OUT, "stats.npz"))
@@ -108,7 +113,15 @@ def main():
     st = dict(np.load(path)) if os.path.exists(path) else {}
     for name, R, chunk, t_f in plan:
         t0 = time.time()
-        E = sample(name, R, t_f, workers, chunk)
+        if a.extend and name + "_E" in st:
+            old = st[name + "_E"].astype(np.float64)
+            jobs = [(name, r, min(r + chunk, a.extend), t_f) for r in range(old.size, a.extend, chunk)]
+            E = np.concatenate([old, np.empty(a.extend - old.size)])
+            with Pool(workers) as pool:
+                for r0, e in pool.imap_unordered(_chunk, jobs):
+                    E[r0:r0 + e.size] = e
+        else:
+            E = sample(name, R, t_f, workers, chunk)
         wall = time.time() - t0
         base = ref[name + "_E"]
         m = min(base.size, E.size)

@@ -10,11 +10,13 @@ and identical to `nmfa_batch` on every seed the two share.
 Criterion, per instance and path: the GPU's p lies inside the reference's
 95% Wilson interval (metrics.py:70-75 defines p).  Success is E <= the
 reference's minimum (SK100, Moebius-100: the best-known energies -730 and
--146) or E <= E*, the reference sample's 10th-percentile energy (G2000,
-K2000: SURVEY 8(d) C4).  The GPU sample is 2-4x the reference's so the
-interval is set by the reference's own sampling error.  The GPU's seeded
-noise is its own counter-based stream, so agreement is
-statistical, not per seed.
+-146) or E <= E* (G2000, K2000).  E* is the 10th-percentile energy of the
+FIRST 4096 reference reads, and the reference's p and
+interval are taken over the reads AFTER those 4096, so the threshold is not
+selected on the sample it is scored on (an empirical quantile scored on its
+own sample sits at 0.10 + its tie mass by construction, which makes the
+interval meaningless).  The GPU's seeded noise is its own counter-based
+stream, so agreement is statistical, not per seed.
 """
 
 import numpy as np
@@ -46,31 +48,39 @@ REF = golden("stats_large.npz")
 CASES = {  # name: (builder, GPU reads, threshold rule, paths)
     "sk100": (lambda: nb.gen_sk(100, 0), 131072, "min", ["small"]),
     "moebius100": (lambda: nb.moebius_ladder(100), 65536, "min", ["small", "sparse"]),
-    "g2000": (lambda: nb.gen_dense_maxcut(2000, 0.01, 7), 8192, "q10", ["dense", "sparse"]),
-    "sk2000": (lambda: nb.gen_sk(2000, 7), 8192, "q10", ["dense"]),
+    "g2000": (lambda: nb.gen_dense_maxcut(2000, 0.01, 7), 32768, "q10", ["dense", "sparse"]),
+    "sk2000": (lambda: nb.gen_sk(2000, 7), 16384, "q10", ["dense"]),
 }
+SELECT = 4096  # reference reads that fix E* for the q10 rule
 
 
-def threshold(e_ref, rule):
-    return float(e_ref.min()) if rule == "min" else float(np.quantile(e_ref, 0.1, method="lower"))
+def reference_success(e_ref, rule):
+    """(threshold, k_ref, n_ref): E* from the first SELECT reads, scored on the rest."""
+    if rule == "min":
+        thr = float(e_ref.min())
+        scored = e_ref
+    else:
+        thr = float(np.quantile(e_ref[:SELECT], 0.1, method="lower"))
+        scored = e_ref[SELECT:] if e_ref.size > SELECT else e_ref
+    return thr, int(np.count_nonzero(scored <= thr + 1e-9)), int(scored.size)
 
 
 @pytest.mark.parametrize("name,path", [(k, p) for k, v in CASES.items() for p in v[3]])
 def test_success_probability_inside_reference_ci(name, path):
     make, reads, rule, _ = CASES[name]
     e_ref = REF[name + "_E"].astype(np.float64)
-    thr = threshold(e_ref, rule)
-    k_ref = int(np.count_nonzero(e_ref <= thr + 1e-9))
-    lo, hi = O.wilson_interval(k_ref, e_ref.size)
+    thr, k_ref, n_ref = reference_success(e_ref, rule)
+    lo, hi = O.wilson_interval(k_ref, n_ref)
     p = make()
     p.device_handle().set_path(path)
     res = nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads)
     e = res.energies.cpu().numpy()
     k = int(np.count_nonzero(e <= thr + 1e-9))
     pg = k / e.size
-    pool = (k + k_ref) / (e.size + e_ref.size)
-    z = (pg - k_ref / e_ref.size) / np.sqrt(pool * (1 - pool) * (1 / e.size + 1 / e_ref.size))
-    print(f"{name}[{path}] E_thr={thr:.0f} p_gpu={pg:.4f} ({k}/{e.size}) p_ref={k_ref / e_ref.size:.4f} "
+    pool = (k + k_ref) / (e.size + n_ref)
+    z = (pg - k_ref / n_ref) / np.sqrt(pool * (1 - pool) * (1 / e.size + 1 / n_ref))
+    print(f"{name}[{path}] E_thr={thr:.0f} p_gpu={pg:.4f} ({k}/{e.size}) p_ref={k_ref / n_ref:.4f} "
+          f"({k_ref}/{n_ref}) "
           f"ref 95% CI=[{lo:.4f}, {hi:.4f}] z={z:+.2f} mean E gpu={e.mean():.2f} ref={e_ref.mean():.2f}")
     if rule == "min":   # nothing below the best-known energy
         assert e.min() >= thr - 1e-9
