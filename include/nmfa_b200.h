@@ -214,6 +214,16 @@ int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_ou
 int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy_host,
                       int64_t* degeneracy_host, int8_t* config_host);
 
+/* The reference's own per-run noise on the device (the
+ * replay mode of nmfa_batch): run r (global index r0 + r) gets
+ * noise_stream(seed + r0 + r).standard_normal(count) * sigma (solver.py:
+ * 182-185, 236-241: numpy Philox4x64-10 keyed [seed + r0 + r, 2], numpy's
+ * ziggurat), count = t_f * n in C order, into noise_dev [n_reads][count] f32
+ * and/or noise64_dev (f64).  Bitwise numpy's draws in f32; f64 tail draws may
+ * differ by an ulp (device log1p).  Asynchronous on `stream`. */
+int nmfa_reference_noise(uint64_t seed, int64_t r0, int64_t n_reads, int64_t count, double sigma,
+                         float* noise_dev, double* noise64_dev, void* stream);
+
 const char* nmfa_last_error(void);
 const char* nmfa_version(void);
 /* Number of kernels the last nmfa_plan_run on this thread enqueued. */

@@ -44,6 +44,7 @@ SIGNATURES = {
     "nmfa_version": (ctypes.c_char_p, []),
     "nmfa_last_launch_count": (_i64, []),
     "nmfa_debug_guard_check": (_i64, []),
+    "nmfa_reference_noise": (_i32, [_u64, _i64, _i64, _i64, _f64, _p, _p, _p]),
     "nmfa_problem_create_sk_device": (_i32, [_i64, _u64, _i64, _i64, _i32, ctypes.POINTER(_p)]),
     "nmfa_plan_run_sweeps": (_i32, [_p, _u64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "nmfa_plan_image_info": (_i32, [_p, ctypes.POINTER(_p), ctypes.POINTER(_p),

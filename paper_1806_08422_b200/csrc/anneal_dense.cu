@@ -96,6 +96,7 @@ struct DenseState {
   int np = 0, kp = 0, kblocks = 0, k_last_sub = 0, pairs = 0;
   int slice_lo = 0, slice_hi = 0;  // k-slices of the image this device writes
   long long Rp = 0;
+  long long slice_b = 0;           // bytes per k-slice of an operand image (Rp * 256 + pad)
   uint8_t* lo_img = nullptr;
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
@@ -124,6 +125,7 @@ struct DenseStepArgs {
   int kblocks, k_last_sub;
   int n, brows, row_lo;    // B image rows (row shard of J) and the shard's first spin
   long long R, Rp;
+  long long slice_b;       // bytes per k-slice of an image (a multiple of 128)
   int t_begin, t_end, t_f;  // sweeps [t_begin, t_end) of t_f; energy pass after t_f-1
   int energy_pass;
   float alpha, oma, sigma;
@@ -277,6 +279,15 @@ __device__ __forceinline__ void fence_acq_rel_gpu() {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// readiness mailbox between the prefetch thread and the TMA producer of a CTA
+__device__ __forceinline__ unsigned long long ld_acquire_cta_smem(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_smem(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
+}
 
 // Persistent multi-sweep kernel.  Every pair walks its static tile list once
 // per sweep t in [t_begin, t_end) and then (energy_pass) once more in energy
@@ -300,6 +311,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   __shared__ __align__(8) uint64_t full_bar[kDStages], empty_bar[kDStages];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_slot;
+  // readiness mailbox: (tile step << 16) | k-order slices of that step known ready
+  __shared__ __align__(8) unsigned long long pf_ready;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_rank();
@@ -321,6 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       mbar_init(&tempty_bar[s], 2 * kDEpiWarps);
     }
     fence_mbar_init();
+    pf_ready = 0;
   }
   if (warp == kWarpAlloc) tmem_alloc_pair(&tmem_slot, 2 * kAccCols);
   tc_fence_before();
@@ -332,17 +346,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int it = 0;
+      unsigned long long seen = 0;  // last pf_ready value observed
       const uint64_t pol_keep = policy_evict_last();
       for (int ph = 0; ph < n_phases; ++ph) {
         const int t = a.t_begin + ph;
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
-        int known_m = -1, known = 0;  // leading k-order entries of block known_m ready this sweep
         for (int j = j0; j < j1; ++j) {
           const DenseTile tl = a.tiles[j];
-          if (tl.m_blk != known_m) {
-            known_m = tl.m_blk;
-            known = ph > 0 ? 0 : a.kblocks;
-          }
           const int half = tl.nlen >> 1;
           const int arow = tl.m_blk * 256 + (int)cta * 128;
           const int brow = tl.n0 - a.row_lo + (int)cta * half;  // row within this shard of J
@@ -352,26 +362,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           unsigned long long* t2 = (a.tl2 && cta == 0 && jglob < 64) ? a.tl2 + ((blockIdx.x >> 1) * 64 + jglob) * 8 : nullptr;
           if (t2) t2[0] = gtimer();
           long long wempty = 0;
+          const unsigned long long step = (unsigned long long)jglob << 16;
           for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
             const int kb = kord ? kord[ki] : ki;
-            if (ki >= known) {
-              // slices of block m for sweep t were written by sweep t-1: poll the next
-              // (up to) 8 entries of the k order with independent relaxed loads
-              const int qb = tl.m_blk * a.kblocks;
-              while (known <= ki) {
-                unsigned v[8];
-                const int cnt = min(8, a.kblocks - known);
-#pragma unroll
-                for (int x = 0; x < 8; ++x)
-                  if (x < cnt) v[x] = ld_relaxed_gpu(a.ready + qb + (kord ? kord[known + x] : known + x));
-                int adv = 0;
-#pragma unroll
-                for (int x = 0; x < 8; ++x)
-                  if (x < cnt && adv == x && v[x] >= (unsigned)ph * a.kneed[qb + (kord ? kord[known + x] : known + x)]) ++adv;
-                known += adv;
-                if (known <= ki) __nanosleep(20);
-              }
-              fence_acq_rel_gpu();
+            if (seen < step + (unsigned long long)(ki + 1)) {
+              // the slices of block m for sweep t were written by sweep t-1: the
+              // prefetch thread (alloc warp) polls the readiness counters ahead of
+              // this thread and posts progress in pf_ready, so a block switch costs
+              // one shared-memory load instead of a round of L2 polls and fences
+              do {
+                seen = ld_acquire_cta_smem(&pf_ready);
+                if (seen < step + (unsigned long long)(ki + 1)) __nanosleep(20);
+              } while (seen < step + (unsigned long long)(ki + 1));
               fence_proxy_async_global();
             }
             if (ki == a.kblocks - 1 && a.trace && blockIdx.x == 0 && jglob < 512)
@@ -396,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
 #endif
             uint8_t* st = smem + (size_t)s * kDStageBytes;
-            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * a.Rp + arow) * 2, fb, pol_keep);
+            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * (a.slice_b >> 7) + arow * 2), fb, pol_keep);
 #ifndef NMFA_DBG_NOB
             // J rows of this CTA's half of the tile: ONE box (the per-box TMA cost is
             // ~100 cycles, so the half is never split into power-of-two boxes)
@@ -460,6 +462,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         }
       }
     }
+  } else if (warp == kWarpAlloc) {
+    // ------------------------- readiness prefetch -------------------------
+    // Walks the producer's tile sequence ahead of it.  For sweep t > t_begin a
+    // tile needs every k-slice of its replica block from sweep t-1, tracked
+    // per (block, slice) in `ready` (spins published, summed over the epilogue
+    // warps of all pairs).  Progress is posted as (step << 16) | slices known,
+    // in the tile's K order; a later step's value implies all earlier ones.
+    if (lane == 0) {
+      unsigned long long step = 0;
+      for (int ph = 0; ph < n_phases; ++ph) {
+        int done_m = -1;  // block whose slices are all known ready in this sweep
+        for (int j = j0; j < j1; ++j, ++step) {
+          const DenseTile tl = a.tiles[j];
+          if (ph == 0 || tl.m_blk == done_m) {
+            st_release_cta_smem(&pf_ready, (step << 16) | (unsigned long long)a.kblocks);
+            continue;
+          }
+          const int16_t* kord = a.korder ? a.korder + (size_t)j * a.kblocks : nullptr;
+          const int qb = tl.m_blk * a.kblocks;
+          int known = 0;
+          while (known < a.kblocks) {
+            unsigned v[8];
+            const int cnt = min(8, a.kblocks - known);
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+              if (x < cnt) v[x] = ld_relaxed_gpu(a.ready + qb + (kord ? kord[known + x] : known + x));
+            int adv = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+              if (x < cnt && adv == x &&
+                  v[x] >= (unsigned)ph * a.kneed[qb + (kord ? kord[known + x] : known + x)])
+                ++adv;
+            if (adv) {
+              known += adv;
+              fence_acq_rel_gpu();  // acquire the published slices for this CTA
+              st_release_cta_smem(&pf_ready, (step << 16) | (unsigned long long)known);
+            } else {
+              __nanosleep(32);
+            }
+          }
+          done_m = tl.m_blk;
+        }
+      }
+    }
   } else if (warp >= kEpiBase && warp < kEpiBase + kDEpiWarps) {
     // ------------------------- fused NMFA epilogue -------------------------
     // State per (replica r, spin i): hi = fp16(s) lives in the operand image
@@ -501,8 +547,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const int n8 = tl.nlen >> 3;
         const int c_lo = (n8 * hpart / kParts) * 8, c_hi = (n8 * (hpart + 1) / kParts) * 8;
         // byte offset of spins i..i+7 of replica r in an operand image: 32-bit
-        // (plans keep each image below 4 GiB), k-slice stride Rp * 256 bytes
-        const uint32_t slice_bytes = (uint32_t)a.Rp * 256u, row_off32 = (uint32_t)row_off;
+        // (plans keep each image below 4 GiB), k-slice stride slice_b bytes
+        const uint32_t slice_bytes = (uint32_t)a.slice_b, row_off32 = (uint32_t)row_off;
         auto img_off = [&](int i) {
           return (uint32_t)(i >> 7) * slice_bytes + row_off32 + (uint32_t)((i & 127) >> 3) * 128u;
         };
@@ -676,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
 // A image 0 (hi) and the lo image from s0: one thread per (replica, 8-spin
 // core row) writes one 16-byte chunk of each image (padding stays zero).
 __global__ void dense_init_kernel(uint8_t* a_img, uint8_t* lo_img, const float* s0, int n, int kp,
-                                  long long R, long long Rp) {
+                                  long long R, long long Rp, long long slice_b) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)(kp / 8) * Rp) return;
   const long long r = e % Rp;
@@ -686,7 +732,7 @@ __global__ void dense_init_kernel(uint8_t* a_img, uint8_t* lo_img, const float* 
   for (int k = 0; k < 8; ++k) v[k] = (r < R && i0 + k < n) ? s0[r * n + i0 + k] : 0.f;
   uint4 hv, lv;
   split_hilo8<true>(v, hv, lv, false);
-  const long long off = (long long)(i0 >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i0 & 127) >> 3) * 128 +
+  const long long off = (long long)(i0 >> 7) * slice_b + (r >> 3) * 2048 + ((i0 & 127) >> 3) * 128 +
                         (r & 7) * 16;
   *reinterpret_cast<uint4*>(a_img + off) = hv;
   *reinterpret_cast<uint4*>(lo_img + off) = lv;
@@ -823,7 +869,11 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->kblocks = ds->kp / kBK;
   ds->k_last_sub = (n - (ds->kblocks - 1) * kBK + 15) / 16;
   ds->Rp = (pl->R + 255) / 256 * 256;
-  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  // experiment knob NMFA_SLICE_PAD: extra 128-byte lines between k-slices, so
+  // the slices of one replica block are not a power-of-two stride apart
+  static const char* pad_env = getenv("NMFA_SLICE_PAD");
+  ds->slice_b = ds->Rp * 256 + 128LL * (pad_env ? std::max(0, atoi(pad_env)) : 0);
+  const size_t img_bytes = (size_t)ds->kblocks * ds->slice_b;
   if (img_bytes >= (1ULL << 32)) {  // the epilogue addresses images with 32-bit offsets
     set_error("dense plan: n x replicas too large for one plan (state image >= 4 GiB); "
               "split the replicas over several calls (r0)");
@@ -873,7 +923,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
   // debug knob NMFA_TILE_ORDER: mmajor (contiguous m-major runs), sorted (the
   // same runs ordered by spin within each pair), spin (spin-major dealing)
   static const char* order_env = getenv("NMFA_TILE_ORDER");
-  const std::string order = order_env ? order_env : "mmajor";
+  const std::string order = order_env ? order_env : "skew";
   std::vector<DenseTile> mmaj;
   mmaj.reserve(T);
   for (long long m = 0; m < mb; ++m)
@@ -884,7 +934,60 @@ int dense_plan_alloc(nmfa_plan* pl) {
   std::vector<DenseTile> tiles;
   tiles.reserve(T);
   std::vector<int> off(pairs + 1, 0);
-  if (order == "block") {
+  // Skewed dealing (default): replica blocks split into an early class E and a
+  // late class L.  Every pair runs its E tiles first and its L tiles last, at
+  // least one of each, so an E block's tiles sit in positions [0, S-2] and an
+  // L block's in [1, S-1] (S = tiles per pair).  Position 0 of sweep t+1 then
+  // consumes only E blocks, finished at least one tile-time before the sweep
+  // boundary, and no pair waits for another pair's last tile (m-major runs made
+  // every sweep start wait ~20 us for the previous sweep's last epilogues,
+  // profiles/r02/dense_schedule.log).  Within a class the tiles are m-major
+  // runs, as before.  K order and results are unchanged.
+  std::vector<long long> cnt(pairs), ecnt(pairs, 0);
+  for (int q = 0; q < pairs; ++q) cnt[q] = T * (q + 1) / pairs - T * q / pairs;
+  bool skew = order == "skew" || order_env == nullptr;
+  long long mbE = 0;
+  if (skew) {
+    // E = the first mbE blocks; find a split the per-pair bounds can realise
+    long long lo_sum = 0, hi_sum = 0;
+    for (int q = 0; q < pairs; ++q) {
+      lo_sum += cnt[q] >= 2 ? 1 : 0;
+      hi_sum += cnt[q] >= 2 ? cnt[q] - 1 : cnt[q];
+    }
+    skew = false;
+    for (long long dm = 0; dm <= mb && !skew; ++dm)
+      for (long long cand : {mb / 2 - dm, (mb + 1) / 2 + dm})
+        if (!skew && cand >= 1 && cand < mb && cand * tpm >= lo_sum && cand * tpm <= hi_sum) {
+          mbE = cand;
+          skew = true;
+        }
+    if (skew) {
+      long long need = mbE * tpm, sum = 0;
+      for (int q = 0; q < pairs; ++q) {
+        ecnt[q] = cnt[q] >= 2 ? std::max(1LL, cnt[q] / 2) : 0;
+        sum += ecnt[q];
+      }
+      for (int q = 0; sum < need && q < 4 * pairs; ++q) {  // raise E counts up to cnt - 1
+        const int i = q % pairs;
+        const long long cap = cnt[i] >= 2 ? cnt[i] - 1 : cnt[i];
+        if (ecnt[i] < cap) ++ecnt[i], ++sum;
+      }
+      for (int q = 0; sum > need && q < 4 * pairs; ++q) {  // lower them down to 1 (0 for single tiles)
+        const int i = pairs - 1 - q % pairs;
+        const long long floor_ = cnt[i] >= 2 ? 1 : 0;
+        if (ecnt[i] > floor_) --ecnt[i], --sum;
+      }
+      skew = sum == need;
+    }
+  }
+  if (skew) {
+    long long je = 0, jl = mbE * tpm;  // cursors into the m-major list (E blocks first)
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int)tiles.size();
+      for (long long k = 0; k < ecnt[q]; ++k) tiles.push_back(mmaj[je++]);
+      for (long long k = ecnt[q]; k < cnt[q]; ++k) tiles.push_back(mmaj[jl++]);
+    }
+  } else if (order == "block") {
     // m-major list dealt round-robin: at position j the pairs hold whole replica
     // blocks (~pairs / tiles-per-block of them), so block m's sweep-t tiles all
     // finish at one position and its sweep-(t+1) tiles run a full sweep later
@@ -987,7 +1090,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
 
   int err;
   for (int b = 0; b < 2; ++b)
-    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
+    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * (ds->slice_b >> 7), 256)))
       return err;
   // one B tensor map per distinct tile width (balanced widths: at most two)
   {
@@ -1028,12 +1131,12 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
     return NMFA_ERR_STATE;
   }
   int64_t launches = 1;
-  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  const size_t img_bytes = (size_t)ds->kblocks * ds->slice_b;
   if (t_begin == 0) {
     if (s0) {
       const long long tot = (long long)(ds->kp / 8) * ds->Rp;
       dense_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-          ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp);
+          ds->a_img[0], ds->lo_img, s0, (int)p->n, ds->kp, pl->R, ds->Rp, ds->slice_b);
       NMFA_LAUNCH_CHECK();
       ++launches;
     } else {  // S(0) = 0 (solver.py:200-201)
@@ -1056,6 +1159,7 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   a.row_lo = (int)p->row_lo;
   a.R = pl->R;
   a.Rp = ds->Rp;
+  a.slice_b = ds->slice_b;
   a.t_begin = t_begin;
   a.t_end = t_end;
   a.t_f = pl->t_f;
@@ -1175,7 +1279,7 @@ int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int 
     set_error("not a dense plan");
     return NMFA_ERR_STATE;
   }
-  const size_t img_bytes = (size_t)ds->kp * ds->Rp * 2;
+  const size_t img_bytes = (size_t)ds->kblocks * ds->slice_b;
   if (world < 1 || world > kMaxPeers + 1 || rank < 0 || rank >= world) {
     set_error("fused exchange needs 1 <= world <= 8 and 0 <= rank < world");
     return NMFA_ERR_ARG;
@@ -1202,7 +1306,7 @@ int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int 
   }
   int err;
   for (int b = 0; b < 2; ++b)
-    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * ds->Rp * 2, 256)))
+    if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * (ds->slice_b >> 7), 256)))
       return err;
   ds->n_peers = 0;
   for (int g = 0; g < world; ++g) {
@@ -1238,7 +1342,7 @@ int dense_image_info(const nmfa_plan* pl, void** img0, void** img1, int64_t* sli
   }
   *img0 = ds->a_img[0];
   *img1 = ds->a_img[1];
-  *slice_bytes = ds->Rp * 256;
+  *slice_bytes = ds->slice_b;
   *n_slices = ds->kblocks;
   *slice_lo = ds->slice_lo;
   *slice_hi = ds->slice_hi;
@@ -1247,12 +1351,12 @@ int dense_image_info(const nmfa_plan* pl, void** img0, void** img1, int64_t* sli
 
 // cfg[r][i] = sign of the fp16 +-1 sign image
 __global__ void read_config_kernel(const uint8_t* img, int8_t* cfg, int n, long long R,
-                                   long long Rp) {
+                                   long long slice_b) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)n * R) return;
   const long long r = e / n;
   const int i = (int)(e - r * n);
-  const long long off = (long long)(i >> 7) * Rp * 256 + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
+  const long long off = (long long)(i >> 7) * slice_b + (r >> 3) * 2048 + ((i & 127) >> 3) * 128 +
                         (r & 7) * 16 + (i & 7) * 2;
   const __half h = *reinterpret_cast<const __half*>(img + off);
   cfg[e] = __half2float(h) < 0.f ? (int8_t)-1 : (int8_t)1;
@@ -1266,7 +1370,7 @@ int dense_read_config(const nmfa_plan* pl, int8_t* cfg, cudaStream_t st) {
   }
   const long long tot = pl->p->n * pl->R;
   read_config_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-      ds->a_img[pl->t_f & 1], cfg, (int)pl->p->n, pl->R, ds->Rp);
+      ds->a_img[pl->t_f & 1], cfg, (int)pl->p->n, pl->R, ds->slice_b);
   NMFA_LAUNCH_CHECK();
   add_launches(1);
   return NMFA_OK;

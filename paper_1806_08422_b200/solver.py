@@ -420,16 +420,87 @@ def _results(problem, res, params, record_trajectory):
                       trajectory=trajs[r]) for r in range(R)]
 
 
-def nmfa_run(problem, params, record_trajectory=False, device=0):
-    """Full anneal from all-zero spins; deterministic given (problem, seed)."""
-    res = sample(problem, params, 1, device=device, record_trajectory=record_trajectory)
+NOISE_MODES = ("device", "reference")
+REPLAY_CHUNK_BYTES = 1 << 30   # device noise buffer per replay chunk (float32)
+
+
+def reference_noise(seed, n_runs, t_f, n, sigma, *, r0=0, device=0):
+    """The reference's per-run noise, generated on the GPU (refnoise.cu).
+
+    Returns a (n_runs, t_f, n) float32 device tensor whose row r is
+    noise_stream(seed + r0 + r).standard_normal((t_f, n)) * sigma -- exactly
+    what `_run` draws for run seed + r0 + r (solver.py:236-241), rounded to
+    float32 (bitwise numpy's draws at that precision)."""
+    import torch
+
+    out = torch.empty((int(n_runs), int(t_f), int(n)), dtype=torch.float32,
+                      device=torch.device("cuda", device))
+    stream = torch.cuda.current_stream(out.device)
+    _native.check(_native.load().nmfa_reference_noise(
+        int(seed) & MASK64, int(r0), int(n_runs), int(t_f) * int(n), float(sigma), _native.ptr(out),
+        None, ctypes.c_void_p(stream.cuda_stream)))
+    return out
+
+
+def _replay(problem, params, n_runs, device, record_trajectory):
+    """Seeded anneals on the reference's own noise streams: replica chunks of
+    at most REPLAY_CHUNK_BYTES of device noise, each generated on the GPU and
+    injected through the run_with_noise seam.  One SampleSet for all runs."""
+    import torch
+
+    problem = as_problem(problem)
+    n, t_f = problem.n, int(params.t_f)
+    temps = params.schedule.temperatures(t_f)
+    chunk = max(1, min(n_runs, REPLAY_CHUNK_BYTES // (4 * t_f * n)))
+    parts, wall = [], 0.0
+    for c0 in range(0, n_runs, chunk):
+        c = min(chunk, n_runs - c0)
+        nz = reference_noise(params.seed, c, t_f, n, params.sigma, r0=c0, device=device)
+        res = sample(problem, params, c, device=device, noise=nz, temps=temps,
+                     record_trajectory=record_trajectory)
+        parts.append(res)
+        wall += res.wall_clock
+        del nz
+    cat = (lambda xs: torch.cat(xs) if xs[0] is not None else None)
+    return SampleSet(cat([r.configs for r in parts]), cat([r.energies for r in parts]),
+                     int(params.seed), 0, wall, None, cat([r.s_hist for r in parts]),
+                     cat([r.e_hist for r in parts]))
+
+
+def _check_noise_mode(noise):
+    if noise not in NOISE_MODES:
+        raise ValueError(f"noise must be one of {NOISE_MODES}, got {noise!r}")
+
+
+def nmfa_run(problem, params, record_trajectory=False, device=0, noise="device"):
+    """Full anneal from all-zero spins; deterministic given (problem, seed).
+
+    noise="reference" replays the reference's own stream for params.seed, so
+    the run follows `nmfa.nmfa_run(problem, params)` step for step."""
+    _check_noise_mode(noise)
+    if noise == "reference":
+        res = _replay(problem, params, 1, device, record_trajectory)
+    else:
+        res = sample(problem, params, 1, device=device, record_trajectory=record_trajectory)
     return _results(problem, res, params, record_trajectory)[0]
 
 
-def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, device=0):
-    """n_runs independent anneals; run k uses seed params.seed + k (solver.py:262-280)."""
+def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, device=0,
+               noise="device"):
+    """n_runs independent anneals; run k uses seed params.seed + k (solver.py:262-280).
+
+    noise="device" (default) draws in-kernel counter-based Philox noise keyed
+    by seed + k (statistically equivalent to the reference, not per seed).
+    noise="reference" replays each run's own numpy stream noise_stream(seed +
+    k) generated on the GPU, so run k is comparable per
+    seed with the reference's run k -- slower (the streams are sequential and
+    are injected in replica chunks)."""
     n_runs = int(n_runs)
     if n_runs < 1:
         raise ValueError(f"n_runs must be at least 1, got {n_runs}")
-    res = sample(problem, params, n_runs, device=device, record_trajectory=record_trajectory)
+    _check_noise_mode(noise)
+    if noise == "reference":
+        res = _replay(problem, params, n_runs, device, record_trajectory)
+    else:
+        res = sample(problem, params, n_runs, device=device, record_trajectory=record_trajectory)
     return _results(problem, res, params, record_trajectory)

@@ -148,3 +148,12 @@ def test_toroidal_grid_generator():
     assert np.array_equal(p.edge_weights, q.edge_weights)
     with pytest.raises(ValueError):
         nb.toroidal_grid(2, 5, 0)
+
+
+def test_noise_mode_is_validated_before_any_device_work():
+    import paper_1806_08422_b200 as nb
+    p = nb.moebius_ladder(8)
+    with pytest.raises(ValueError, match="noise must be one of"):
+        nb.nmfa_batch(p, nb.NmfaParams(t_f=10), 4, noise="numpy")
+    with pytest.raises(ValueError, match="noise must be one of"):
+        nb.nmfa_run(p, nb.NmfaParams(t_f=10), noise=None)
