@@ -539,7 +539,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const unsigned long long key = a.key_base + (unsigned long long)r;
         const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
         const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
+#ifdef NMFA_EPI_SPIN  // experiment: plain spinning wait
         mbar_wait(&tfull_bar[slot], use & 1);
+#else
+        mbar_wait_sleep(&tfull_bar[slot], use & 1, 100000u);
+#endif
         if (a.trace && blockIdx.x == 0 && e == 0 && lane == 0 && jj < 512) a.trace[jj * 8 + 4] = clock64();
         tc_fence_after();
         const uint32_t tacc = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)slot * kAccCols;
