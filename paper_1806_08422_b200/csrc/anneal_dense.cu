@@ -81,7 +81,11 @@ constexpr int kEpiBase = 0;
 constexpr int kWarpProducer = kDEpiWarps, kWarpMma = kDEpiWarps + 1, kWarpAlloc = kDEpiWarps + 2;
 #endif
 constexpr uint32_t kATile = 128 * kBK * 2;     // 128 rows x 128 k fp16 = 32 KB
-constexpr uint32_t kBTileMax = 128 * kBK * 2;  // <= 128 rows (N/2) x 128 k
+#ifndef NMFA_DMAXW
+#define NMFA_DMAXW 16  // widest tile in 16-spin units (experiment: 12 makes room for a 4th stage)
+#endif
+constexpr int kMaxW = NMFA_DMAXW;
+constexpr uint32_t kBTileMax = 8 * kMaxW * kBK * 2;  // <= 8 * kMaxW rows (N/2) x 128 k
 constexpr uint32_t kDStageBytes = kATile + kBTileMax;
 constexpr uint32_t kAccCols = 256;
 constexpr size_t kDSmemBytes = (size_t)kDStages * kDStageBytes + 1024;
@@ -902,9 +906,9 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->slice_lo = (int)(p->row_lo / kBK);
   ds->slice_hi = (int)((p->row_hi + kBK - 1) / kBK);
   const long long upm = p->brows / 16, mb = ds->Rp / 256;
-  int best_w = 16;
+  int best_w = kMaxW;
   double best_cost = 1e300;
-  for (int w = 1; w <= 16; ++w) {
+  for (int w = 1; w <= kMaxW; ++w) {
     const long long tpm = (upm + w - 1) / w, T = tpm * mb;
     const long long pairs_used = std::min<long long>(sms / 2, T);
     const double per_slice = std::max(64.0 * w, 563.0 + 22.6 * w);
@@ -915,7 +919,7 @@ int dense_plan_alloc(nmfa_plan* pl) {
     }
   }
   static const char* w_env = getenv("NMFA_TILE_W");  // experiment: force the tile width
-  if (w_env && atoi(w_env) >= 1 && atoi(w_env) <= 16) best_w = atoi(w_env);
+  if (w_env && atoi(w_env) >= 1 && atoi(w_env) <= kMaxW) best_w = atoi(w_env);
   const long long tpm = (upm + best_w - 1) / best_w, T = tpm * mb;
   const int pairs = (int)std::min<long long>(sms / 2, T);
   ds->pairs = pairs;

@@ -3,8 +3,8 @@ leg 3): "ground-state success probability per instance falls within the
 reference's binomial confidence interval".
 
 Reference samples: tests/golden/stats_large.npz (make_golden_stats.py) --
-SK100 65,536 reads, Moebius-100 32,768, G2000 and the K2000 stand-in 4,096
-each, produced from the reference's own per-run noise streams and arithmetic
+SK100 65,536 reads, Moebius-100 32,768, G2000 32,768 and the K2000 stand-in
+16,384, produced from the reference's own per-run noise streams and arithmetic
 and identical to `nmfa_batch` on every seed the two share.
 
 Criterion, per instance and path: the GPU's p lies inside the reference's
