@@ -77,9 +77,24 @@ int nmfa_problem_create_csr(int64_t n, const int64_t* indptr, const int64_t* ind
                             nmfa_problem_t** out);
 /* A complete +-1 graph (SK) from packed sign bits: bit (i*n + j) of the
  * row-major bitmap (word b>>5, bit b&31) set -> J_ij = +1, clear -> -1, read
- * for i < j (1/64 of a float64 J). */
+ * for i < j (1/64 of a float64 J).  Up to 4096 spins the host builds the
+ * edge list (every path and the edge-list energy); beyond that this is
+ * nmfa_problem_create_bits_device(n, bits, h, 0, n, ...). */
 int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits_host, const double* h_host,
                                    int32_t device, nmfa_problem_t** out);
+
+/* The bit-packed +-1 device format: the same bitmap is
+ * uploaded (n^2/8 bytes; 512 MiB at n = 65,536) and expanded ON THE DEVICE
+ * into the dense path's fp16 J image of rows [row_lo, row_hi) -- no
+ * n(n-1)/2-entry host edge list, so user instances reach the row-sharded
+ * sizes of BASELINE config 5 (problem.py:25-116 otherwise needs ~50 GB of
+ * host arrays there).  normalizers_safe_i = sqrt(h_i^2 + n - 1)
+ * (problem.py:90-95).  Dense path only; energies come from the tensor-core
+ * energy pass (nmfa_energy included, exact).  Row shards as in
+ * nmfa_problem_create_sk_device. */
+int nmfa_problem_create_bits_device(int64_t n, const uint32_t* sign_bits_host, const double* h_host,
+                                    int64_t row_lo, int64_t row_hi, int32_t device,
+                                    nmfa_problem_t** out);
 int nmfa_problem_destroy(nmfa_problem_t* p);
 int nmfa_problem_get_info(const nmfa_problem_t* p, nmfa_problem_info_t* info);
 /* Synthetic Sherrington-Kirkpatrick instance generated ON DEVICE (BASELINE
@@ -203,6 +218,13 @@ int nmfa_best_of(const double* energy_dev, int64_t n, double* best_energy_dev,
  * (GsetParseError): NMFA_ERR_ARG with "line N: <message>" in nmfa_last_error. */
 int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_out,
                     int64_t* edges_i, int64_t* edges_j, double* weights, int64_t cap);
+
+/* Instance text straight to a device problem, no host-language layer: the
+ * native parse above (same errors and messages), then nmfa_problem_create on
+ * the parsed couplers (load_gset + IsingProblem, gset.py:35-96 and
+ * problem.py:25-116, in one call for a non-Python host). */
+int nmfa_problem_create_gset(const char* text, int64_t len, int32_t device,
+                             nmfa_problem_t** out);
 
 /* Exact ground state by exhaustive enumeration: minimum energy over all 2^n
  * configurations and its degeneracy (brute_force_ground, metrics.py:53-67;

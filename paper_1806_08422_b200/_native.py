@@ -29,6 +29,7 @@ SIGNATURES = {
     "nmfa_problem_destroy": (_i32, [_p]),
     "nmfa_problem_create_dense": (_i32, [_i64, _p, _p, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_create_dense_bits": (_i32, [_i64, _p, _p, _i32, ctypes.POINTER(_p)]),
+    "nmfa_problem_create_bits_device": (_i32, [_i64, _p, _p, _i64, _i64, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_create_csr": (_i32, [_i64, _p, _p, _p, _p, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_get_info": (_i32, [_p, _p]),
     "nmfa_problem_set_path": (_i32, [_p, _i32]),
@@ -55,6 +56,7 @@ SIGNATURES = {
     "nmfa_plan_set_exchange": (_i32, [_p, _p, _p, _i32, _i32, _i64]),
     "nmfa_gset_parse": (_i32, [ctypes.c_char_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                _p, _p, _p, _i64]),
+    "nmfa_problem_create_gset": (_i32, [ctypes.c_char_p, _i64, _i32, ctypes.POINTER(_p)]),
     "nmfa_ground_state": (_i32, [_p, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_i64), _p]),
 }
 

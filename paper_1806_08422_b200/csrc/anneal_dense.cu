@@ -836,6 +836,75 @@ __global__ void sk_image_kernel(uint8_t* img, long long n, int brows, long long 
                  pack_half2(v[6], v[7]));
 }
 
+// J image rows [row_lo, row_lo + brows) of a complete +-1 instance given as
+// packed sign bits (the bit-packed device format): bit
+// a * n + b (a < b, row-major over the n x n matrix, 32 per uint32 word,
+// LSB first) set means J_ab = +1, clear means -1.  One thread per (row,
+// 8 consecutive k); J is symmetric, so (i, k) reads bit (min, max).
+__global__ void bits_image_kernel(uint8_t* img, const uint32_t* __restrict__ bits, long long n,
+                                  int brows, long long row_lo, int kp) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per_row = kp / 8;
+  if (e >= (long long)brows * per_row) return;
+  const int lrow = (int)(e / per_row);
+  const int k0 = (int)(e - (long long)lrow * per_row) * 8;
+  const long long i = row_lo + lrow;
+  float v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const long long k = k0 + c;
+    v[c] = 0.f;
+    if (i < n && k < n && k != i) {
+      const unsigned long long b = (unsigned long long)(i < k ? i : k) * (unsigned long long)n +
+                                   (unsigned long long)(i < k ? k : i);
+      v[c] = ((__ldg(bits + (b >> 5)) >> (b & 31)) & 1u) ? 1.f : -1.f;
+    }
+  }
+  const long long off = (long long)(k0 >> 7) * brows * 256 + (lrow >> 3) * 2048 +
+                        ((k0 & 127) >> 3) * 128 + (lrow & 7) * 16;
+  *reinterpret_cast<uint4*>(img + off) =
+      make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+                 pack_half2(v[6], v[7]));
+}
+
+int dense_problem_from_bits(nmfa_problem* p, const uint32_t* d_bits) {
+  const int kp = (int)((p->n + kBK - 1) / kBK * kBK);
+  const size_t bytes = (size_t)kp * p->brows * 2;
+  p->j_dense_bytes = bytes;
+  NMFA_CUDA_TRY(cudaMalloc(&p->d_j_dense, bytes));
+  NMFA_CUDA_TRY(cudaMemset(p->d_j_dense, 0, bytes));
+  const long long tot = (long long)p->brows * (kp / 8);
+  bits_image_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(
+      reinterpret_cast<uint8_t*>(p->d_j_dense), d_bits, p->n, p->brows, p->row_lo, kp);
+  NMFA_LAUNCH_CHECK();
+  NMFA_CUDA_TRY(cudaDeviceSynchronize());
+  return NMFA_OK;
+}
+
+// Exact energies of arbitrary +-1 configurations through the dense kernel's
+// tensor-core energy pass alone (t_begin = t_end = 0): the configurations are
+// written as the A image (hi = +-1, lo = 0) and E = 1/2 j_scale c.(J c) + h.c
+// is reduced in the epilogue.  For device-built problems, which have no edge
+// list.  cfg: int8 [R][n] of +-1 (R = the plan's replica count).
+__global__ void cfg_to_float_kernel(const int8_t* __restrict__ cfg, long long count,
+                                    float* __restrict__ s) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < count) s[k] = cfg[k] < 0 ? -1.f : 1.f;
+}
+
+int dense_energy_only(const nmfa_plan* pl, const int8_t* cfg, double* energy, cudaStream_t st) {
+  const long long count = pl->p->n * pl->R;
+  float* s0 = nullptr;
+  NMFA_CUDA_TRY(cudaMallocAsync(&s0, (size_t)count * sizeof(float), st));
+  cfg_to_float_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(cfg, count, s0);
+  int err = cudaGetLastError() == cudaSuccess ? NMFA_OK : NMFA_ERR_CUDA;
+  if (!err)
+    err = dense_run_sweeps(pl, 0, nullptr, s0, nullptr, nullptr, nullptr, energy, 0, 0, true, st);
+  cudaFreeAsync(s0, st);
+  if (!err) add_launches(1);
+  return err;
+}
+
 int dense_problem_generate_sk(nmfa_problem* p, uint64_t seed) {
   const int kp = (int)((p->n + kBK - 1) / kBK * kBK);
   const size_t bytes = (size_t)kp * p->brows * 2;

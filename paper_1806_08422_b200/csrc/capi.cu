@@ -396,7 +396,9 @@ int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits, const d
   if (!out || !sign_bits) return arg_error("NULL argument");
   *out = nullptr;
   if (n < 2) return arg_error("a complete +-1 graph needs n >= 2, got " + std::to_string(n));
-  if (n > (int64_t)1 << 17) return arg_error("spin count too large for the host edge list");
+  // beyond kBitsHostMaxN spins the n(n-1)/2-entry host edge list is not built:
+  // the bits go to the device and are expanded there (dense path only)
+  if (n > kBitsHostMaxN) return nmfa_problem_create_bits_device(n, sign_bits, h, 0, n, device, out);
   const int64_t m = n * (n - 1) / 2;
   std::vector<int64_t> ei((size_t)m), ej((size_t)m);
   std::vector<double> w((size_t)m);
@@ -409,6 +411,83 @@ int nmfa_problem_create_dense_bits(int64_t n, const uint32_t* sign_bits, const d
       w[k] = ((sign_bits[b >> 5] >> (b & 31)) & 1u) ? 1.0 : -1.0;
     }
   return nmfa_problem_create(n, m, ei.data(), ej.data(), w.data(), h, device, out);
+  NMFA_API_END
+}
+
+int nmfa_problem_create_bits_device(int64_t n, const uint32_t* sign_bits, const double* h,
+                                    int64_t row_lo, int64_t row_hi, int32_t device,
+                                    nmfa_problem_t** out) {
+  NMFA_API_BEGIN
+  if (!out || !sign_bits) return arg_error("NULL argument");
+  *out = nullptr;
+  if (n < 2) return arg_error("a complete +-1 graph needs n >= 2, got " + std::to_string(n));
+  if (n > (int64_t)1 << 20) return arg_error("spin count too large for the dense path");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi)
+    return arg_error("row shard must satisfy 0 <= row_lo < row_hi <= n");
+  if (row_lo % 128 != 0 || (row_hi % 128 != 0 && row_hi != n))
+    return arg_error("row shard boundaries must be multiples of 128 (or n)");
+  auto* p = new nmfa_problem();
+  p->device = device;
+  p->n = n;
+  p->n_edges = n * (n - 1) / 2;
+  p->density = 1.0;
+  p->is_dense = true;
+  p->path = NMFA_PATH_DENSE;
+  p->int_weights = true;
+  p->j_exact = true;
+  p->j_scale = 1.0;
+  p->device_generated = true;
+  p->h.assign(n, 0.0);
+  if (h)
+    for (int64_t i = 0; i < n; ++i) {
+      if (!std::isfinite(h[i])) {
+        delete p;
+        return arg_error("fields must be finite");
+      }
+      p->h[i] = h[i];
+      p->has_field = p->has_field || h[i] != 0.0;
+    }
+  // normalizers_safe = sqrt(h^2 + sum_j J_ij^2) (problem.py:90-95): n - 1 unit couplers per row
+  p->norm_safe.resize(n);
+  double max_h = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    p->norm_safe[i] = std::sqrt(p->h[i] * p->h[i] + (double)(n - 1));
+    max_h = std::max(max_h, std::fabs(p->h[i]));
+  }
+  p->max_row_abs = (double)(n - 1);
+  p->row_lo = row_lo;
+  p->row_hi = row_hi;
+  p->brows = (int32_t)((row_hi - row_lo + 15) / 16 * 16);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete p;
+    return arg_error("invalid CUDA device " + std::to_string(device));
+  }
+  int err = NMFA_OK;
+  uint32_t* d_bits = nullptr;
+  do {
+    p->np = (int32_t)((n + 15) / 16 * 16);
+    std::vector<float> invn(p->np, 0.f), hn(p->np, 0.f);
+    for (int64_t i = 0; i < n; ++i) {
+      invn[i] = (float)(1.0 / p->norm_safe[i]);
+      hn[i] = (float)(p->h[i] / p->norm_safe[i]);
+    }
+    if ((err = upload(&p->d_invn, invn.data(), invn.size()))) break;
+    if ((err = upload(&p->d_hn, hn.data(), hn.size()))) break;
+    if ((err = upload(&p->d_h, p->h.data(), p->h.size()))) break;
+    const size_t words = (size_t)(((unsigned long long)n * (unsigned long long)n + 31) / 32);
+    if ((err = upload(&d_bits, sign_bits, words))) break;
+    err = dense_problem_from_bits(p, d_bits);
+  } while (0);
+  if (d_bits) cudaFree(d_bits);
+  cudaSetDevice(prev);
+  if (err) {
+    nmfa_problem_destroy(p);
+    return err;
+  }
+  *out = p;
+  return NMFA_OK;
   NMFA_API_END
 }
 
@@ -709,6 +788,22 @@ int nmfa_gset_parse(const char* text, int64_t len, int64_t* n_out, int64_t* m_ou
   NMFA_API_END
 }
 
+int nmfa_problem_create_gset(const char* text, int64_t len, int32_t device,
+                             nmfa_problem_t** out) {
+  NMFA_API_BEGIN
+  if (!text || len < 0 || !out) return arg_error("NULL argument");
+  *out = nullptr;
+  int64_t n = 0, m = 0;
+  int err = gset_parse(text, len, &n, &m, nullptr, nullptr, nullptr, 0);
+  if (err) return err;
+  std::vector<int64_t> ei((size_t)m), ej((size_t)m);
+  std::vector<double> w((size_t)m);
+  if ((err = gset_parse(text, len, &n, &m, ei.data(), ej.data(), w.data(), m))) return err;
+  std::vector<double> h((size_t)n, 0.0);  // the instance format has no field column (gset.py:99-109)
+  return nmfa_problem_create(n, m, ei.data(), ej.data(), w.data(), h.data(), device, out);
+  NMFA_API_END
+}
+
 int nmfa_ground_state(const nmfa_problem_t* p, int32_t max_n, double* energy,
                       int64_t* degeneracy, int8_t* config) {
   NMFA_API_BEGIN
@@ -938,10 +1033,30 @@ int nmfa_energy(const nmfa_problem_t* p, const int8_t* cfg, int64_t n_cfg, doubl
                 void* stream) {
   NMFA_API_BEGIN
   if (!p || !cfg || !energy) return arg_error("NULL argument");
-  if (p->device_generated)
-    return arg_error("a device-generated problem has no edge list; its energies come from "
-                     "the anneal's tensor-core energy pass");
   if (n_cfg < 1) return arg_error("need at least one configuration");
+  if (p->device_generated) {
+    // no edge list on the device: the dense kernel's exact tensor-core energy
+    // pass on the given configurations (integer J, |J c| < 2^24)
+    if (dense_is_sharded(p))
+      return arg_error("a row-sharded problem holds only its rows of J; its energies come from "
+                       "the sharded protocol (sharded.py)");
+    if (!dense_energy_exact(p)) return state_error("tensor-core energies are not exact here");
+    const double one = 1.0;
+    nmfa_plan_t* pl = nullptr;
+    int err = nmfa_plan_create(p, n_cfg, 1, &one, 0.15, 0.15, &pl);
+    if (err) return err;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    err = dense_energy_only(pl, cfg, energy, (cudaStream_t)stream);
+    if (!err && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
+      set_error("CUDA error in the tensor-core energy pass");
+      err = NMFA_ERR_CUDA;
+    }
+    cudaSetDevice(prev);
+    nmfa_plan_destroy(pl);
+    return err;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int prev = 0;
   cudaGetDevice(&prev);

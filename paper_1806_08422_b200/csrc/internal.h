@@ -28,6 +28,9 @@ void add_launches(int64_t k);
 #define NMFA_LAUNCH_CHECK() NMFA_CUDA_TRY(cudaGetLastError())
 
 constexpr int kSmallMaxN = 256;  // persistent path keeps J (<=128 KB fp16) in SMEM
+// nmfa_problem_create_dense_bits builds the host edge list up to this many
+// spins; larger complete +-1 instances are expanded on the device
+constexpr int64_t kBitsHostMaxN = 4096;
 
 }  // namespace nmfa
 
@@ -143,6 +146,8 @@ int dense_image_info(const nmfa_plan* pl, void** img0, void** img1, int64_t* sli
                      int32_t* n_slices, int32_t* slice_lo, int32_t* slice_hi);
 int dense_read_config(const nmfa_plan* pl, int8_t* cfg, cudaStream_t st);
 int dense_problem_generate_sk(nmfa_problem* p, uint64_t seed);
+int dense_problem_from_bits(nmfa_problem* p, const uint32_t* d_bits);
+int dense_energy_only(const nmfa_plan* pl, const int8_t* cfg, double* energy, cudaStream_t st);
 int dense_plan_alloc(nmfa_plan* pl);
 void dense_plan_free(nmfa_plan* pl);
 int dense_problem_upload(nmfa_problem* p, const std::vector<float>& jdense_rowmajor);

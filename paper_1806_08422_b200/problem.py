@@ -213,9 +213,86 @@ class _DeviceProblem:
             pass
 
 
+def pack_sign_bits(J):
+    """Pack the signs of a symmetric +-1 matrix into the bitmap of the
+    bit-packed device format: bit i * n + j (i < j, row-major, 32 per uint32,
+    LSB first) set iff J_ij > 0.  1/64 of the float64 matrix."""
+    J = np.asarray(J)
+    n = J.shape[0]
+    if J.ndim != 2 or J.shape != (n, n):
+        raise ValueError("J must be a square matrix")
+    iu, ju = np.triu_indices(n, 1)
+    if np.any(np.abs(J[iu, ju]) != 1.0) or not np.array_equal(J[iu, ju], J[ju, iu]):
+        raise ValueError("J must be symmetric with +-1 off-diagonal entries")
+    flat = np.zeros(n * n, dtype=np.uint8)
+    flat[iu * n + ju] = J[iu, ju] > 0
+    pad = (-flat.size) % 32
+    bits = np.packbits(np.concatenate([flat, np.zeros(pad, np.uint8)]), bitorder="little")
+    return bits.view(np.uint32).copy()
+
+
+class PackedSignProblem:
+    """A complete +-1 instance (SK, K2000-style MAX-CUT) held as packed sign
+    bits: the bit-packed device format.  The bitmap is
+    expanded on the GPU into the dense path's J image
+    (nmfa_problem_create_bits_device); no n(n-1)/2 host edge list exists, so
+    n may reach the row-sharded sizes (65,536: a 512 MiB bitmap).  Accepted by
+    sample / nmfa_batch / nmfa_run / energies like an IsingProblem; energies
+    come from the exact tensor-core energy pass."""
+
+    def __init__(self, n, bits, h=None):
+        n = _spin_count(n)
+        if n < 2:
+            raise ValueError("a complete +-1 graph needs n >= 2")
+        bits = np.ascontiguousarray(bits, dtype=np.uint32)
+        if bits.ndim != 1 or bits.size < (n * n + 31) // 32:
+            raise ValueError(f"bitmap needs {(n * n + 31) // 32} uint32 words for n = {n}")
+        self.n, self.bits, self.h = n, bits, _fields(n, h)
+        self._handles = {}
+        self._hlock = threading.Lock()
+
+    @classmethod
+    def from_dense(cls, J, h=None):
+        return cls(np.asarray(J).shape[0], pack_sign_bits(J), h)
+
+    @property
+    def num_edges(self):
+        return self.n * (self.n - 1) // 2
+
+    @property
+    def w_total(self):
+        """Sum of the couplings (cut_value's W_total): #(+1) - #(-1) over i < j."""
+        words = (self.n * self.n + 31) // 32
+        plus = int(np.unpackbits(self.bits[:words].view(np.uint8)).sum())
+        return float(2 * plus - self.num_edges)
+
+    def coupling(self, i, j):
+        """J_ij from the bitmap (i != j)."""
+        a, b = (i, j) if i < j else (j, i)
+        k = a * self.n + b
+        return 1.0 if (int(self.bits[k >> 5]) >> (k & 31)) & 1 else -1.0
+
+    def device_handle(self, device=0):
+        device = int(device)
+        with self._hlock:
+            h = self._handles.get(device)
+            if h is None:
+                out = ctypes.c_void_p()
+                hv = np.ascontiguousarray(self.h, dtype=np.float64)
+                _native.check(_native.load().nmfa_problem_create_bits_device(
+                    self.n, _native.ptr(self.bits), _native.ptr(hv), 0, self.n, device,
+                    ctypes.byref(out)))
+                h = _DeviceProblem(out, device)
+                self._handles[device] = h
+            return h
+
+    def device_info(self, device=0):
+        return self.device_handle(device).info()
+
+
 def as_problem(obj):
     """Accept our IsingProblem or any object with the reference's fields."""
-    if isinstance(obj, IsingProblem):
+    if isinstance(obj, (IsingProblem, PackedSignProblem)):
         return obj
     cached = getattr(obj, "_nmfa_b200_problem", None)
     if cached is not None:

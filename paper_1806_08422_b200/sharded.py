@@ -144,10 +144,13 @@ class ShardedResult:
 
 
 class RowShardedSK(ShardProtocol):
-    """Synthetic SK instance with J row-sharded over the ranks of `group`."""
+    """SK instance with J row-sharded over the ranks of `group`: the synthetic
+    on-device generator (`seed`), or a user's complete +-1 instance given as
+    packed sign bits (`bits`, the bit-packed device format of
+    problem.PackedSignProblem; each rank expands only its rows)."""
 
     def __init__(self, n, seed, n_reads, params=None, group=None, device=None, shard=None,
-                 exchange="nccl"):
+                 exchange="nccl", bits=None, h=None):
         import torch
         import torch.distributed as dist
 
@@ -164,9 +167,18 @@ class RowShardedSK(ShardProtocol):
         self.row_lo, self.row_hi = row_shard(n, self.world, self.rank) if self.world > 1 else (0, n)
         lib = _native.load()
         out = ctypes.c_void_p()
-        _native.check(lib.nmfa_problem_create_sk_device(self.n, int(seed) & MASK64, self.row_lo,
-                                                        self.row_hi, self.device,
-                                                        ctypes.byref(out)))
+        if bits is None:
+            _native.check(lib.nmfa_problem_create_sk_device(self.n, int(seed) & MASK64,
+                                                            self.row_lo, self.row_hi, self.device,
+                                                            ctypes.byref(out)))
+        else:
+            self._bits = np.ascontiguousarray(bits, dtype=np.uint32)
+            self._h = None if h is None else np.ascontiguousarray(h, dtype=np.float64)
+            if self._bits.size < (self.n * self.n + 31) // 32:
+                raise ValueError("bitmap too short for n")
+            _native.check(lib.nmfa_problem_create_bits_device(
+                self.n, _native.ptr(self._bits), _native.ptr(self._h), self.row_lo, self.row_hi,
+                self.device, ctypes.byref(out)))
         self.problem = out
         self.temps = np.ascontiguousarray(self.params.schedule.temperatures(self.params.t_f))
         plan = ctypes.c_void_p()

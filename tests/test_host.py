@@ -157,3 +157,23 @@ def test_noise_mode_is_validated_before_any_device_work():
         nb.nmfa_batch(p, nb.NmfaParams(t_f=10), 4, noise="numpy")
     with pytest.raises(ValueError, match="noise must be one of"):
         nb.nmfa_run(p, nb.NmfaParams(t_f=10), noise=None)
+
+
+def test_pack_sign_bits_layout_and_validation():
+    rng = np.random.default_rng(0)
+    n = 37
+    J = np.triu(np.where(rng.random((n, n)) < 0.5, -1.0, 1.0), 1)
+    J = J + J.T
+    bits = nb.pack_sign_bits(J)
+    assert bits.dtype == np.uint32 and bits.size == (n * n + 31) // 32
+    p = nb.PackedSignProblem(n, bits)
+    for i, j in [(0, 1), (3, 30), (36, 2), (10, 11)]:
+        assert p.coupling(i, j) == J[i, j]
+        b = min(i, j) * n + max(i, j)
+        assert ((int(bits[b >> 5]) >> (b & 31)) & 1) == (J[i, j] > 0)
+    iu = np.triu_indices(n, 1)
+    assert p.w_total == J[iu].sum() and p.num_edges == n * (n - 1) // 2
+    with pytest.raises(ValueError, match="symmetric"):
+        nb.pack_sign_bits(np.triu(J))
+    with pytest.raises(ValueError, match="uint32 words"):
+        nb.PackedSignProblem(n, bits[:-1])
