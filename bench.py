@@ -334,9 +334,14 @@ def measure_statistics(nb, dev, workload, last_energies):
         thr = float(np.quantile(e_ref[:4096], q, method="lower"))
         return thr, (e_ref[4096:] if e_ref.size > 4096 else e_ref)
 
-    for name, expr, reads, q in cases:
+    # Moebius-100 also on the CSR/ELL gather path BASELINE config 2 names (the router
+    # sends n <= 256 to the on-chip small kernel, which is faster)
+    cases.append(("moebius100", "moebius_ladder(100)", 32768, None, "sparse"))
+    for name, expr, reads, q, *force in cases:
         thr, e_ref = reference_success(ref[name + "_E"].astype(np.float64), q)
         p = eval("nb." + expr, {"nb": nb})
+        if force:
+            p.device_handle(dev.index).set_path(force[0])
         ev = (torch_event(), torch_event())
         nb.sample(p, nb.NmfaParams(t_f=1000, seed=0), reads, device=dev.index)   # warm the plan
         ev[0].record()
@@ -345,7 +350,7 @@ def measure_statistics(nb, dev, workload, last_energies):
         ev[1].synchronize()
         e = res.energies.cpu().numpy()
         wall = ev[0].elapsed_time(ev[1]) * 1e-3
-        out[name] = {"threshold_E": thr, "threshold": "reference minimum" if q is None else
+        out[name + ("_" + force[0] if force else "")] = {"threshold_E": thr, "threshold": "reference minimum" if q is None else
                      "10th percentile of the first 4096 reference reads; reference p over the rest", "path": p.device_info(dev.index)["path"],
                      "spin_updates_per_s": p.n * reads * 1000 / wall, "seed": 0,
                      **compare_p(int(np.count_nonzero(e <= thr + 1e-9)), reads,
@@ -713,6 +718,20 @@ def run_ours(args):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_value = world * n * R * t_f * e2e_steps / float(et.item())
 
+    # ---- the reference-compatible Python entry itself: nb.nmfa_batch returns the
+    # reference's list[RunResult] (float64 +-1 configs, one dataclass per run)
+    e2e_py = None
+    if rank == 0 and world == 1:
+        nb.nmfa_batch(p, params, R, device=local)          # warm
+        t0 = time.perf_counter()
+        runs = nb.nmfa_batch(p, params, R, device=local)
+        py_wall = time.perf_counter() - t0
+        e2e_py = {"value": n * R * t_f / py_wall, "unit": "spin-updates/s",
+                  "wall_s": py_wall, "runs": len(runs),
+                  "api": "nb.nmfa_batch(problem, params, n_runs) -> list[RunResult] (the reference's "
+                         "return type: float64 configs, one dataclass per run; solver.py:262-280)"}
+        del runs
+
     tts = None
     if rank == 0 and not args.no_tts:
         tts = measure_tts_sk100(nb, dev, args.no_cpu_baseline)
@@ -745,6 +764,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(temps.nbytes),
                     "d2h_bytes_per_step": int(R * n + R * 8),
                     "api": "nmfa_anneal_host (C ABI, host buffers)"},
+            **({"e2e_python_api": e2e_py} if e2e_py else {}),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "tts99_sk100": tts,
