@@ -543,8 +543,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         const unsigned long long key = a.key_base + (unsigned long long)r;
         const PhiloxKey K = philox_schedule((uint32_t)key, (uint32_t)(key >> 32));
         const long long row_off = (r >> 3) * 2048 + (r & 7) * 16;
-#ifdef NMFA_EPI_SPIN  // experiment: plain spinning wait
+#if defined(NMFA_EPI_SPIN)  // experiment: plain spinning wait
         mbar_wait(&tfull_bar[slot], use & 1);
+#elif defined(NMFA_EPI_BACKOFF)  // experiment: test_wait + nanosleep(NMFA_EPI_BACKOFF) ns
+        mbar_wait_backoff(&tfull_bar[slot], use & 1, NMFA_EPI_BACKOFF);
 #else
         mbar_wait_sleep(&tfull_bar[slot], use & 1, 100000u);
 #endif

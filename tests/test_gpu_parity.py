@@ -2,8 +2,9 @@
 
 Tolerances: the device state is fp32 with an fp16
 tensor-core operand, the reference is float64, so trajectories under the
-same injected noise agree to |dS| <= 2e-2 with identical final signs wherever
-the reference spin is not within 2e-2 of zero; energies are bit-exact for
+same injected noise agree to |dS| <= 2e-3 (fp16-operand paths) / 1e-5 (fp32
+sparse path) with identical final signs wherever the reference spin is not
+within that bound of zero; energies are bit-exact for
 integer weights; seeded statistics agree within binomial confidence bounds.
 """
 
@@ -63,8 +64,12 @@ def test_injected_noise_trajectory_matches_reference(G, name, path):
     t_f, seed = int(T[name + "_tf"]), int(T[name + "_seed"])
     noise = O.run_noise(seed, t_f, p.n, 0.15)
     s, tr = nb.run_with_noise(p, O.temperatures(t_f), noise, 0.15, record_trajectory=True)
-    assert_traj_close(s, T[name + "_s"])
-    assert_traj_close(tr.spins[-10:], T[name + "_s_hist_last10"])
+    # SURVEY 8(c) proposes max|dS| <= 1e-2 for N <= 500; measured on these fixtures
+    # (tools/traj_fixture_maxds.py): <= 9.6e-4 with the fp16 GEMM operand (small,
+    # dense), <= 2.5e-6 on the fp32 sparse path, so the bounds are 2e-3 and 1e-5
+    tol = 1e-5 if path == "sparse" else 2e-3
+    assert_traj_close(s, T[name + "_s"], tol)
+    assert_traj_close(tr.spins[-10:], T[name + "_s_hist_last10"], tol)
     # trajectory energies are exact energies of the GPU's own rounded spins
     op = oprob(G, name)
     want = O.energies(op, O.sign_round(tr.spins))
