@@ -409,6 +409,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             tma2d_pair(smem_u32(st + kATile), half == a.bhalf1 ? &tmB1 : &tmB0, 0,
                        (kb * a.brows + brow) * 2, fb, pol_keep);
 #endif
+#ifdef NMFA_L2_PREFETCH  // experiment: pull the A box NMFA_L2_PREFETCH k-slices ahead into L2
+            if (ki + NMFA_L2_PREFETCH < a.kblocks) {
+              const int kb2 = kord ? kord[ki + NMFA_L2_PREFETCH] : ki + NMFA_L2_PREFETCH;
+              asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                               reinterpret_cast<uint64_t>(tmA)),
+                           "r"(0), "r"((int)(kb2 * (a.slice_b >> 7) + arow * 2))
+                           : "memory");
+            }
+#endif
           }
           if (a.trace && blockIdx.x == 0 && jglob < 512)
             a.trace[jglob * 8 + 7] = wempty;  // cycles the producer waited for a free stage
