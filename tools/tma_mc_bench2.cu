@@ -14,7 +14,10 @@
 
 using namespace nmfa;
 
-constexpr int kStages = 4;
+#ifndef STAGES
+#define STAGES 4
+#endif
+constexpr int kStages = STAGES;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -117,8 +120,8 @@ void run(void* buf, long long lines, int tile_lines, unsigned long long* clk) {
   double mean = 0;
   for (int i = 0; i < grid; ++i) mean += (double)h[i] / grid;
   const double per = mean / iters;
-  printf("cluster %d %-9s tile %3d KB (box %2d KB)  err=%d  %7.1f clk/stage  %6.1f B/clk/SM delivered, %6.1f B/clk/SM issued\n",
-         CS, MC ? "multicast" : "unicast", tile_lines / 8, box / 8, (int)err, per, tile_lines * 128 / per,
+  printf("stages %d cluster %d %-9s tile %3d KB (box %2d KB)  err=%d  %7.1f clk/stage  %6.1f B/clk/SM delivered, %6.1f B/clk/SM issued\n",
+         kStages, CS, MC ? "multicast" : "unicast", tile_lines / 8, box / 8, (int)err, per, tile_lines * 128 / per,
          box * 128 / per);
 }
 
@@ -133,7 +136,7 @@ int main() {
   cudaMemset(buf, 1, bytes);
   unsigned long long* clk;
   cudaMalloc(&clk, 148 * 8);
-  for (int tl : {128, 224, 256}) {
+  for (int tl : {128, 224}) {
     run<1, false>(buf, lines, tl, clk);
     run<2, false>(buf, lines, tl, clk);
     run<2, true>(buf, lines, tl, clk);
