@@ -266,6 +266,35 @@ class PackedSignProblem:
         plus = int(np.unpackbits(self.bits[:words].view(np.uint8)).sum())
         return float(2 * plus - self.num_edges)
 
+    @property
+    def normalizers_safe(self):
+        """sqrt(h_i^2 + n - 1): every spin has n - 1 unit couplers (problem.py:90-95)."""
+        return np.sqrt(self.h * self.h + float(self.n - 1))
+
+    def _rows(self, i0, i1):
+        """Dense +-1 rows [i0, i1) of J from the bitmap (0 on the diagonal)."""
+        n = self.n
+        ii = np.arange(i0, i1)[:, None]
+        jj = np.arange(n)[None, :]
+        a, b = np.minimum(ii, jj), np.maximum(ii, jj)
+        k = a * n + b
+        bit = (self.bits[k >> 5] >> (k & 31).astype(np.uint32)) & 1
+        J = np.where(bit == 1, 1.0, -1.0)
+        J[ii == jj] = 0.0
+        return J
+
+    def matvec(self, s):
+        """J @ s, unpacking the bitmap in row blocks (mean_field's sum_j J_ij s_j)."""
+        s = np.asarray(s, dtype=np.float64)
+        out = np.empty(self.n)
+        step = max(1, (1 << 22) // self.n)
+        for i0 in range(0, self.n, step):
+            out[i0:i0 + step] = self._rows(i0, min(self.n, i0 + step)) @ s
+        return out
+
+    def _build_csr(self):  # normalizers(); the bitmap has no CSR, only its norms
+        return None, None, None, np.sqrt(self.h * self.h + float(self.n - 1))
+
     def coupling(self, i, j):
         """J_ij from the bitmap (i != j)."""
         a, b = (i, j) if i < j else (j, i)

@@ -177,3 +177,16 @@ def test_pack_sign_bits_layout_and_validation():
         nb.pack_sign_bits(np.triu(J))
     with pytest.raises(ValueError, match="uint32 words"):
         nb.PackedSignProblem(n, bits[:-1])
+
+
+def test_packed_sign_problem_host_helpers():
+    rng = np.random.default_rng(3)
+    n = 50
+    J = np.triu(np.where(rng.random((n, n)) < 0.5, -1.0, 1.0), 1)
+    J = J + J.T
+    h = rng.integers(-2, 3, n).astype(float)
+    p = nb.PackedSignProblem.from_dense(J, h)
+    s = rng.uniform(-1, 1, n)
+    assert np.allclose(nb.mean_field(p, s), h + J @ s, atol=1e-12)
+    assert np.allclose(nb.normalizers(p), np.sqrt(h * h + (J * J).sum(1)), atol=1e-12)
+    assert np.allclose(p.normalizers_safe, np.sqrt(h * h + n - 1))
