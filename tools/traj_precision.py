@@ -51,11 +51,24 @@ def run(p, noise, temps, variant, alpha=0.15):
     invn = (1.0 / p.normalizers_safe).astype(np.float32)[:, None]
     S = np.zeros((p.n, R), dtype=np.float32)
     q = {"f16op": lambda s: s.astype(np.float16).astype(np.float32), "bf16op": bf16,
-         "f32op": lambda s: s}[variant]
+         "f32op": lambda s: s, "f16op_lo8": lambda s: s.astype(np.float16).astype(np.float32),
+         "f16op_lo16": lambda s: s.astype(np.float16).astype(np.float32)}[variant]
+
+    def store(S):  # the state as the dense kernel stores it between sweeps
+        if variant == "f16op_lo16":   # hi = fp16(s), lo = fp16(s - hi)  (today's kernel)
+            hi = S.astype(np.float16).astype(np.float32)
+            return hi + (S - hi).astype(np.float16).astype(np.float32)
+        if variant == "f16op_lo8":    # hi = fp16(s), lo = int8 in units of ulp(hi)/254
+            hi = S.astype(np.float16)
+            ulp = np.spacing(np.abs(hi)).astype(np.float32)
+            ulp = np.where(ulp == 0, np.float32(2.0 ** -24), ulp)
+            qv = np.clip(np.rint((S - hi.astype(np.float32)) / ulp * 254.0), -127, 127)
+            return (hi.astype(np.float32) + qv.astype(np.float32) * ulp / 254.0).astype(np.float32)
+        return S
     for t in range(len(temps)):
         phi = (J @ q(S)) * invn + noise[:, t, :].T.astype(np.float32)
         sh = -np.tanh(phi * np.float32(1.0 / temps[t]))
-        S = (np.float32(alpha) * sh + np.float32(1.0 - alpha) * S).astype(np.float32)
+        S = store((np.float32(alpha) * sh + np.float32(1.0 - alpha) * S).astype(np.float32))
     return S.T.astype(np.float64)
 
 
