@@ -70,3 +70,36 @@ def test_version_and_errors_are_strings():
     assert b"sm_100a" in lib.nmfa_version()
     lib.nmfa_plan_destroy(None)
     assert isinstance(lib.nmfa_last_error(), bytes)
+
+
+def test_round2_entry_points_validate_before_cuda():
+    out = ctypes.c_void_p()
+    buf = np.zeros(16, np.float32)
+    # nmfa_reference_noise (the replay mode's device stream)
+    assert lib.nmfa_reference_noise(0, 0, 0, 10, 0.15, _native.ptr(buf), None, None) == ARG
+    assert "positive" in err()
+    assert lib.nmfa_reference_noise(0, 0, 4, 10, 0.15, None, None, None) == ARG
+    assert "no output buffer" in err()
+    assert lib.nmfa_reference_noise(0, 0, 4, 10, -1.0, _native.ptr(buf), None, None) == ARG
+    # nmfa_problem_create_bits_device (the bit-packed device format)
+    bits = np.zeros(8, np.uint32)
+    assert lib.nmfa_problem_create_bits_device(16, None, None, 0, 16, 0, ctypes.byref(out)) == ARG
+    assert lib.nmfa_problem_create_bits_device(1, _native.ptr(bits), None, 0, 1, 0,
+                                               ctypes.byref(out)) == ARG
+    assert "n >= 2" in err()
+    assert lib.nmfa_problem_create_bits_device(16, _native.ptr(bits), None, 8, 16, 0,
+                                               ctypes.byref(out)) == ARG
+    assert "multiples of 128" in err()
+    assert lib.nmfa_problem_create_bits_device(16, _native.ptr(bits), None, 0, 17, 0,
+                                               ctypes.byref(out)) == ARG
+    h = np.full(16, np.inf)
+    assert lib.nmfa_problem_create_bits_device(16, _native.ptr(bits), _native.ptr(h), 0, 16, 0,
+                                               ctypes.byref(out)) == ARG
+    assert "finite" in err()
+    # nmfa_problem_create_gset: parse errors carry the reference's line numbers
+    bad = b"3 2\n1 2 1\n1 9 1\n"
+    assert lib.nmfa_problem_create_gset(bad, len(bad), 0, ctypes.byref(out)) == ARG
+    assert err().startswith("line 3")
+    assert lib.nmfa_problem_create_gset(None, 0, 0, ctypes.byref(out)) == ARG
+    # the product library reports that it has no guard allocator
+    assert lib.nmfa_debug_guard_check() == -1
