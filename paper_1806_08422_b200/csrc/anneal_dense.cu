@@ -260,15 +260,27 @@ __device__ __forceinline__ void st_hint(void* ptr, uint4 v, uint64_t) {
 #else
 __device__ __forceinline__ uint4 ld_hint(const void* ptr, uint64_t pol) {
   uint4 v;
+#ifdef NMFA_EPI_NOALLOC  // experiment: state loads do not allocate in L1 (the SMEM/L1 SRAM)
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+#else
   asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(ptr), "l"(pol));
+#endif
   return v;
 }
 __device__ __forceinline__ void st_hint(void* ptr, uint4 v, uint64_t pol) {
+#ifdef NMFA_EPI_STCS  // experiment: streaming (.cs) stores, no L2 policy
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+#else
   asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
+#endif
 }
 #endif
 
@@ -713,13 +725,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
         if (a.trace && blockIdx.x == 0 && lane == 0 && jj < 512) atomicMax(&a.trace[jj * 8 + 5], clock64());
         if (a.tl2 && lane == 0 && jj < 64) atomicMax(&a.tl2[((blockIdx.x >> 1) * 64 + jj) * 8 + 4], gtimer());
         if (lane == 0) {
-          // one release fence orders the warp's TMEM reads (tcgen05 fence + __syncwarp
-          // above) and its state stores before both the accumulator-free arrive and
-          // the readiness counters; the consumers acquire and fence the async proxy
+#ifdef NMFA_EPI_FENCE_FIRST  // round-1 order: the accumulator-free arrive waits for the stores
           fence_release_gpu();
           mbar_remote_arrive_relaxed(slot ? leader_tempty1 : leader_tempty0);
+#else
+          // The accumulator slot is free once this warp's TMEM reads are done
+          // (tcgen05.wait::ld, tcgen05 fence + __syncwarp above): the arrive does not
+          // wait for the state stores.  Only the readiness counters need them, so the
+          // gpu-scope release fence (which waits for the stores to be acknowledged)
+          // now sits on that path alone and no longer delays the MMA of tile j+2.
+          mbar_remote_arrive_relaxed(slot ? leader_tempty1 : leader_tempty0);
+#endif
           if (!energy_phase && c_hi > c_lo) {
-            // publish this warp's rows x columns for the next sweep (spin-quarters)
+            // publish this warp's rows x columns for the next sweep (spin-quarters):
+            // release its state stores (all lanes', ordered by the __syncwarp) first;
+            // the consumers acquire and fence the async proxy
+#ifndef NMFA_EPI_FENCE_FIRST
+            fence_release_gpu();
+#endif
             fence_proxy_async_global();
             const int s_lo = tl.n0 + c_lo, s_hi = tl.n0 + c_hi;
             for (int kb = s_lo >> 7; kb <= (s_hi - 1) >> 7; ++kb)
