@@ -102,8 +102,9 @@ __device__ __forceinline__ uint4_ philox4x32_10(uint32_t c0, uint32_t c1, uint32
 #endif
 #pragma unroll
   for (int i = 0; i < NMFA_PHILOX_ROUNDS; ++i) {
-    // 32-bit hi/lo products (no 64-bit register pairs: under the epilogue's
-    // register cap the paired IMAD.WIDE form costs an extra copy per product)
+    // 32-bit hi/lo products: the compiler pairs them into one IMAD.WIDE.U32 where
+    // registers allow (small kernel: 4 instructions per round with hoisted round
+    // keys); under the dense epilogue's register cap it keeps IMAD.HI + IMAD
     const uint32_t h0 = __umulhi(M0, c0), l0 = M0 * c0;
     const uint32_t h1 = __umulhi(M1, c2), l1 = M1 * c2;
     const uint32_t n0 = h1 ^ c1 ^ (K.k0 + (uint32_t)i * 0x9E3779B9u);
