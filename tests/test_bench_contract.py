@@ -47,3 +47,12 @@ def test_workloads_are_declared(wl):
     sys.path.insert(0, REPO)
     import bench
     assert wl in bench.WORKLOADS and bench.metric_name(wl).endswith(wl)
+
+
+def test_reference_arm_nonzero_rank_exits_quietly():
+    """Under torchrun the reference arm runs on rank 0 only; other ranks exit 0
+    with no output and no process group."""
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference"],
+                         cwd=REPO, capture_output=True, text=True, timeout=120,
+                         env=dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1"))
+    assert out.returncode == 0 and not out.stdout.strip(), out.stdout + out.stderr
