@@ -52,12 +52,23 @@ def run(p, noise, temps, variant, alpha=0.15):
     S = np.zeros((p.n, R), dtype=np.float32)
     q = {"f16op": lambda s: s.astype(np.float16).astype(np.float32), "bf16op": bf16,
          "f32op": lambda s: s, "f16op_lo8": lambda s: s.astype(np.float16).astype(np.float32),
-         "f16op_lo16": lambda s: s.astype(np.float16).astype(np.float32)}[variant]
+         "f16op_lo16": lambda s: s.astype(np.float16).astype(np.float32),
+         "f16op_sr16": lambda s: s.astype(np.float16).astype(np.float32)}[variant]
+    rng = np.random.default_rng(12345)
 
     def store(S):  # the state as the dense kernel stores it between sweeps
         if variant == "f16op_lo16":   # hi = fp16(s), lo = fp16(s - hi)  (today's kernel)
             hi = S.astype(np.float16).astype(np.float32)
             return hi + (S - hi).astype(np.float16).astype(np.float32)
+        if variant == "f16op_sr16":   # fp16 state, stochastic rounding (no residual)
+            lo = S.astype(np.float16)
+            lo32 = lo.astype(np.float32)
+            nxt = np.where(S >= lo32, np.nextafter(lo, np.float16(np.inf)),
+                           np.nextafter(lo, np.float16(-np.inf))).astype(np.float32)
+            gap = np.abs(nxt - lo32)
+            frac = np.where(gap > 0, np.abs(S - lo32) / np.where(gap > 0, gap, 1), 0)
+            up = rng.random(S.shape) < frac
+            return np.where(up, nxt, lo32).astype(np.float32)
         if variant == "f16op_lo8":    # hi = fp16(s), lo = int8 in units of ulp(hi)/254
             hi = S.astype(np.float16)
             ulp = np.spacing(np.abs(hi)).astype(np.float32)
