@@ -53,13 +53,18 @@ def run(p, noise, temps, variant, alpha=0.15):
     q = {"f16op": lambda s: s.astype(np.float16).astype(np.float32), "bf16op": bf16,
          "f32op": lambda s: s, "f16op_lo8": lambda s: s.astype(np.float16).astype(np.float32),
          "f16op_lo16": lambda s: s.astype(np.float16).astype(np.float32),
-         "f16op_sr16": lambda s: s.astype(np.float16).astype(np.float32)}[variant]
+         "f16op_sr16": lambda s: s.astype(np.float16).astype(np.float32),
+         "f16op_fx8": lambda s: s.astype(np.float16).astype(np.float32)}[variant]
     rng = np.random.default_rng(12345)
 
     def store(S):  # the state as the dense kernel stores it between sweeps
         if variant == "f16op_lo16":   # hi = fp16(s), lo = fp16(s - hi)  (today's kernel)
             hi = S.astype(np.float16).astype(np.float32)
             return hi + (S - hi).astype(np.float16).astype(np.float32)
+        if variant == "f16op_fx8":    # hi = fp16(s), lo = int8 fixed point, scale 2^-19
+            hi = S.astype(np.float16).astype(np.float32)
+            qv = np.clip(np.rint((S - hi) * np.float32(2.0 ** 19)), -127, 127)
+            return (hi + qv.astype(np.float32) * np.float32(2.0 ** -19)).astype(np.float32)
         if variant == "f16op_sr16":   # fp16 state, stochastic rounding (no residual)
             lo = S.astype(np.float16)
             lo32 = lo.astype(np.float32)
