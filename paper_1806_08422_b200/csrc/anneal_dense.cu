@@ -18,7 +18,10 @@
 // Roles per CTA (640 threads): warps 0-15 epilogue (lane quarter x column
 // part; 4 warps per scheduler to hide the Philox/MUFU latency chains),
 // warp 16 TMA producer, warp 17 MMA issuer (leader CTA only), warp 18 TMEM
-// allocator.  The control roles take the HIGHEST warp ids on purpose: the
+// allocator and then readiness prefetcher (polls the readiness counters of the
+// producer's upcoming tiles and posts them to a shared-memory mailbox, so a
+// switch to a new replica block does not stall the TMA ring on L2 polls and
+// fences).  The control roles take the HIGHEST warp ids on purpose: the
 // warp scheduler favours high ids, and with low ids the producer and MMA
 // issuer starved behind the epilogue warps (measured: 3x longer k-block
 // intervals, see profiles/).  3-stage smem ring (A: one 32 KB box; B: one box
@@ -26,25 +29,31 @@
 // columns so the epilogue of tile j overlaps the MMAs of tile j+1.
 //
 // Persistence: one cooperative launch runs every sweep of the anneal (plus the
-// exact energy pass).  Each pair owns a contiguous run of (replica block, spin
-// range) tiles in m-major order, balanced to whole tiles by a cost model of
-// the MMA and TMA time per k-slice.  Instead of a kernel boundary between
+// exact energy pass).  Each pair owns 3-4 (replica block, spin range) tiles
+// per sweep in a skewed order: the replica blocks are split into an early and
+// a late class, every pair runs its early-class tiles first, so the tiles
+// that start a sweep consume blocks finished a tile-time before the boundary
+// (profiles/r02/dense_schedule.log; widths from a cost model of the MMA and
+// TMA time per k-slice).  Instead of a kernel boundary between
 // sweeps, every warp publishes the k-slices it wrote in per-(replica block,
 // k-slice) readiness counters, and producers wait only for the slices they
 // are about to load; the K order is natural so results do not depend on the
 // schedule, the replica count or the row sharding.
 //
-// Experiment switches (measurements in profiles/r01/, none changes results
-// unless noted):
-//   env NMFA_TILE_ORDER = mmajor | sorted | spin | block | alt | rev  (tile dealing)
-//   env NMFA_KORDER = rotate   (tile starts at its own spin range's k-slice; timing only)
+// Experiment switches (measurements in profiles/r01/ and profiles/r02/, none
+// changes results unless noted):
+//   env NMFA_TILE_ORDER = skew (default) | mmajor | sorted | spin | block | alt | rev
+//   env NMFA_KORDER = rotate | rotm | rotmn  (rotated K orders; timing only)
+//   env NMFA_SLICE_PAD = lines  (pad between image k-slices; layout only)
 //   env NMFA_KORDER = early    (earliest-published-slice-first K order; results
 //                               then depend on the schedule)
 //   env NMFA_TILE_W = 1..16    (force the tile width in 16-spin units)
 //   env NMFA_TRACE / NMFA_TRACE2 / NMFA_TRACE3 = <file>  (clock64/globaltimer traces)
 //   -DNMFA_DBG_NOEPI / NOMEM / NOLOAD / NOLO / NOMATH / NOTMEM / NOMUFU / SPREAD /
 //    PLAINMEM / LOKEEP  (epilogue ablations for timing; results are wrong)
-//   -DNMFA_EPI_PREFETCH, -DNMFA_EPI_WARPS=n, -DNMFA_DSTAGES=n, -DNMFA_ROLES_FIRST
+//   -DNMFA_EPI_PREFETCH, -DNMFA_EPI_WARPS=n, -DNMFA_DSTAGES=n, -DNMFA_DMAXW=n,
+//   -DNMFA_ROLES_FIRST, -DNMFA_EPI_SPIN / NMFA_EPI_BACKOFF=ns, -DNMFA_EPI_FENCE_FIRST,
+//   -DNMFA_EPI_NOALLOC, -DNMFA_EPI_STCS, -DNMFA_L2_PREFETCH=k
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
