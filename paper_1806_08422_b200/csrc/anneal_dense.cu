@@ -660,9 +660,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
 #pragma unroll
               for (int q = 0; q < 8; ++q) lo[8 * h + q] = 0.f;
-#elif !defined(NMFA_DBG_NOMEM)
+#elif !defined(NMFA_DBG_NOMEM) && defined(NMFA_HILO_PLAIN)  // A/B: two converts + FADD
               unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
               unpack_half8(ld_hint(a.lo + off, pol_stream), lo + 8 * h);
+#elif !defined(NMFA_DBG_NOMEM)
+              hilo_sum8(ld_hint(a_cur + off, pol_keep), ld_hint(a.lo + off, pol_stream), ms + 8 * h);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) lo[8 * h + q] = -0.f;  // x + (-0) == x for every x
 #else
 #pragma unroll
               for (int q = 0; q < 8; ++q) { ms[8 * h + q] = 0.01f * q; lo[8 * h + q] = 0.f; }

@@ -402,6 +402,28 @@ __device__ __forceinline__ void unpack_half8(const uint4 v, float f[8]) {
   }
 }
 
+// Mixed-precision FMA (sm_100 FHFMA): f32 d = f16 a * f16 b + f32 c, one
+// instruction where a convert + FADD took two.  Exact for the uses below: the
+// f16 -> f32 conversion is exact and the single rounding is the FADD's.
+__device__ __forceinline__ float fma_f16f16_f32(unsigned short a, unsigned short b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
+// s = hi + lo for 8 values from their packed fp16 words (the dense state):
+// lo is widened once, hi enters through the mixed-precision FMA (hi * 1 + lo).
+__device__ __forceinline__ void hilo_sum8(const uint4 hi, const uint4 lo, float s[8]) {
+  const uint32_t h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+  const unsigned short one = 0x3C00u;  // fp16 1.0
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 lf = __half22float2(*reinterpret_cast<const __half2*>(&l[k]));
+    s[2 * k] = fma_f16f16_f32((unsigned short)(h[k] & 0xFFFFu), one, lf.x);
+    s[2 * k + 1] = fma_f16f16_f32((unsigned short)(h[k] >> 16), one, lf.y);
+  }
+}
+
 // s -> hi = fp16(s), lo = fp16(s - hi) for 8 values (or hi = sign(s) when `sign`)
 // State split for the dense path: hi = fp16(s) is the tensor-core operand,
 // lo = fp16(s - hi) the residual, so hi + lo carries ~22 bits.  (A 2^-11
@@ -421,9 +443,16 @@ __device__ __forceinline__ void split_hilo8(const float s[8], uint4& hi, uint4& 
       b = b < 0.f ? -1.f : 1.f;
     }
     const __half2 hh = __floats2half2_rn(a, b);
+    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+#ifdef NMFA_HILO_PLAIN  // A/B: convert + FADD
     const float2 hf = __half22float2(hh);
     const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
-    h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+#else
+    // s - hi in one mixed-precision FMA per value: hi * (-1) + s (exact product)
+    const unsigned short m1 = 0xBC00u;  // fp16 -1.0
+    const __half2 ll = __floats2half2_rn(fma_f16f16_f32((unsigned short)(h[k] & 0xFFFFu), m1, a),
+                                         fma_f16f16_f32((unsigned short)(h[k] >> 16), m1, b));
+#endif
     l[k] = *reinterpret_cast<const uint32_t*>(&ll);
   }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
