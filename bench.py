@@ -150,8 +150,16 @@ def dist_init():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if os.environ.get("NMFA_BENCH_SHARED_GPU") == "1":
+            # functional check of the N > 1 code path on a one-GPU box: every rank
+            # on cuda:0, host-side gloo collectives (no kernel waits on another
+            # rank); timings from such a run are not bench numbers
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
 
 
@@ -473,7 +481,7 @@ def run_sk65536(args):
             "metric": "spin-updates/s (N*reads*steps/s) on synthetic SK N=65536", "value": value,
             "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f16 operand / f32 state",
+            "vs_baseline": None, "dtype": DTYPES["dense"],
             "data": "synthetic (on-device Philox SK couplings)",
             "config": {"workload": desc, "reads_total": R, "n": n, "t_f": t_f,
                        "parallelism": f"J row-sharded x{world}", "setup_s": setup_s,
