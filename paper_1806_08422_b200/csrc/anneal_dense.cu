@@ -118,6 +118,8 @@ struct DenseState {
   unsigned* d_ready = nullptr;    // per (block, k-slice): spins published this launch
   int n_mblk = 0;
   int n_tiles = 0;
+  std::vector<int> grp_off_base;  // per replica group: start of its tile offsets in d_tile_off
+  std::vector<int> grp_pairs;     // per replica group: CTA pairs of its launch
   int16_t* d_korder = nullptr;     // [tile][kblocks] K order (null: natural)
   CUtensorMap tmA[2];
   CUtensorMap tmB[2];  // B boxes of exactly one tile half (2 x rows lines), the two widths
@@ -1022,10 +1024,34 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->slice_lo = (int)(p->row_lo / kBK);
   ds->slice_hi = (int)((p->row_hi + kBK - 1) / kBK);
   const long long upm = p->brows / 16, mb = ds->Rp / 256;
-  int best_w = kMaxW;
-  double best_cost = 1e300;
+  // L2-aware replica groups: replica blocks never interact, so when the
+  // working set of one sweep (two hi images + lo + J) outgrows L2 the blocks
+  // are split into groups annealed one after another (one persistent launch
+  // each, all t_f sweeps), as long as each group still deals >= 2 tiles to
+  // every pair.  Results are unchanged (natural K order, global replica keys).
+  // profiles/r02/dense_groups.log: N x R beyond L2 fell to 0.65-0.70 of the
+  // sustained peak as one group.  Row-sharded plans advance sweep by sweep
+  // across devices and stay one group.  NMFA_DENSE_GROUPS=k forces k groups,
+  // NMFA_L2_BUDGET_MB sets the budget.
+  const double j_bytes = (double)ds->kp * p->brows * 2.0;
+  auto footprint = [&](long long blocks) { return 3.0 * 2.0 * ds->kp * 256.0 * blocks + j_bytes; };
+  static const char* budget_env = getenv("NMFA_L2_BUDGET_MB");
+  const double budget = (budget_env ? atof(budget_env) : 120.0) * 1e6;
+  const long long tpm_est = (upm + 13) / 14;
+  long long n_groups = 1;
+  if (!dense_is_sharded(p)) {
+    while (footprint((mb + n_groups - 1) / n_groups) > budget) {
+      const long long g2 = n_groups * 2;
+      if (g2 > mb || (mb / g2) * tpm_est < 2LL * (sms / 2)) break;
+      n_groups = g2;
+    }
+  }
+  static const char* groups_env = getenv("NMFA_DENSE_GROUPS");
+  if (groups_env && atoi(groups_env) >= 1) n_groups = std::min<long long>(mb, atoi(groups_env));
+  const long long mb_g = (mb + n_groups - 1) / n_groups;  // largest group
+  int best_w = kMaxW;  double best_cost = 1e300;
   for (int w = 1; w <= kMaxW; ++w) {
-    const long long tpm = (upm + w - 1) / w, T = tpm * mb;
+    const long long tpm = (upm + w - 1) / w, T = tpm * mb_g;
     const long long pairs_used = std::min<long long>(sms / 2, T);
     const double per_slice = std::max(64.0 * w, 563.0 + 22.6 * w);
     const double makespan = (double)((T + pairs_used - 1) / pairs_used) * per_slice;
@@ -1036,110 +1062,125 @@ int dense_plan_alloc(nmfa_plan* pl) {
   }
   static const char* w_env = getenv("NMFA_TILE_W");  // experiment: force the tile width
   if (w_env && atoi(w_env) >= 1 && atoi(w_env) <= kMaxW) best_w = atoi(w_env);
-  const long long tpm = (upm + best_w - 1) / best_w, T = tpm * mb;
-  const int pairs = (int)std::min<long long>(sms / 2, T);
-  ds->pairs = pairs;
-  // Spin-major dealing: sort tiles by (spin tile k, replica block m) and give
-  // position j of pair q the tile q + j*pairs.  Every pair works on the
-  // lowest spins first, so in sweep t the k-slices become ready in the order
-  // the sweep-(t+1) k-loops consume them (natural K order), and the first tile
-  // of a sweep does not wait for the end of the previous one.
-  // debug knob NMFA_TILE_ORDER: mmajor (contiguous m-major runs), sorted (the
-  // same runs ordered by spin within each pair), spin (spin-major dealing)
+  const long long tpm = (upm + best_w - 1) / best_w;
   static const char* order_env = getenv("NMFA_TILE_ORDER");
   const std::string order = order_env ? order_env : "skew";
-  std::vector<DenseTile> mmaj;
-  mmaj.reserve(T);
-  for (long long m = 0; m < mb; ++m)
-    for (long long k = 0; k < tpm; ++k) {  // balanced widths within the block
-      const long long a0 = upm * k / tpm, a1 = upm * (k + 1) / tpm;
-      mmaj.push_back({(int)m, (int)(p->row_lo + a0 * 16), (int)((a1 - a0) * 16), 0});
-    }
-  std::vector<DenseTile> tiles;
-  tiles.reserve(T);
-  std::vector<int> off(pairs + 1, 0);
-  // Skewed dealing (default): replica blocks split into an early class E and a
-  // late class L.  Every pair runs its E tiles first and its L tiles last, at
-  // least one of each, so an E block's tiles sit in positions [0, S-2] and an
-  // L block's in [1, S-1] (S = tiles per pair).  Position 0 of sweep t+1 then
-  // consumes only E blocks, finished at least one tile-time before the sweep
-  // boundary, and no pair waits for another pair's last tile (m-major runs made
-  // every sweep start wait ~20 us for the previous sweep's last epilogues,
-  // profiles/r02/dense_schedule.log).  Within a class the tiles are m-major
-  // runs, as before.  K order and results are unchanged.
-  std::vector<long long> cnt(pairs), ecnt(pairs, 0);
-  for (int q = 0; q < pairs; ++q) cnt[q] = T * (q + 1) / pairs - T * q / pairs;
-  bool skew = order == "skew" || order_env == nullptr;
-  long long mbE = 0;
-  if (skew) {
-    // E = the first mbE blocks; find a split the per-pair bounds can realise
-    long long lo_sum = 0, hi_sum = 0;
-    for (int q = 0; q < pairs; ++q) {
-      lo_sum += cnt[q] >= 2 ? 1 : 0;
-      hi_sum += cnt[q] >= 2 ? cnt[q] - 1 : cnt[q];
-    }
-    skew = false;
-    for (long long dm = 0; dm <= mb && !skew; ++dm)
-      for (long long cand : {mb / 2 - dm, (mb + 1) / 2 + dm})
-        if (!skew && cand >= 1 && cand < mb && cand * tpm >= lo_sum && cand * tpm <= hi_sum) {
-          mbE = cand;
-          skew = true;
-        }
+  std::vector<DenseTile> tiles;            // every group's list, concatenated
+  std::vector<int> off;                    // per group: pairs_g + 1 absolute offsets
+  ds->grp_off_base.clear();
+  ds->grp_pairs.clear();
+  for (long long g = 0; g < n_groups; ++g) {
+    const long long gm0 = mb * g / n_groups, gm1 = mb * (g + 1) / n_groups;
+    const long long T = tpm * (gm1 - gm0);
+    const int pairs = (int)std::min<long long>(sms / 2, T);
+    ds->grp_off_base.push_back((int)off.size());
+    ds->grp_pairs.push_back(pairs);
+    // Spin-major dealing: sort tiles by (spin tile k, replica block m) and give
+    // position j of pair q the tile q + j*pairs.  Every pair works on the
+    // lowest spins first, so in sweep t the k-slices become ready in the order
+    // the sweep-(t+1) k-loops consume them (natural K order), and the first tile
+    // of a sweep does not wait for the end of the previous one.
+    // debug knob NMFA_TILE_ORDER: mmajor (contiguous m-major runs), sorted (the
+    // same runs ordered by spin within each pair), spin (spin-major dealing)
+    std::vector<DenseTile> mmaj;
+    mmaj.reserve(T);
+    for (long long m = gm0; m < gm1; ++m)
+      for (long long k = 0; k < tpm; ++k) {  // balanced widths within the block
+        const long long a0 = upm * k / tpm, a1 = upm * (k + 1) / tpm;
+        mmaj.push_back({(int)m, (int)(p->row_lo + a0 * 16), (int)((a1 - a0) * 16), 0});
+      }
+    std::vector<int> goff(pairs + 1, 0);
+    // Skewed dealing (default): replica blocks split into an early class E and a
+    // late class L.  Every pair runs its E tiles first and its L tiles last, at
+    // least one of each, so an E block's tiles sit in positions [0, S-2] and an
+    // L block's in [1, S-1] (S = tiles per pair).  Position 0 of sweep t+1 then
+    // consumes only E blocks, finished at least one tile-time before the sweep
+    // boundary, and no pair waits for another pair's last tile (m-major runs made
+    // every sweep start wait ~20 us for the previous sweep's last epilogues,
+    // profiles/r02/dense_schedule.log).  Within a class the tiles are m-major
+    // runs, as before.  K order and results are unchanged.
+    const long long mbk = gm1 - gm0;  // blocks in this group
+    std::vector<long long> cnt(pairs), ecnt(pairs, 0);
+    for (int q = 0; q < pairs; ++q) cnt[q] = T * (q + 1) / pairs - T * q / pairs;
+    bool skew = order == "skew" || order_env == nullptr;
+    long long mbE = 0;
     if (skew) {
-      long long need = mbE * tpm, sum = 0;
+      // E = the first mbE blocks; find a split the per-pair bounds can realise
+      long long lo_sum = 0, hi_sum = 0;
       for (int q = 0; q < pairs; ++q) {
-        ecnt[q] = cnt[q] >= 2 ? std::max(1LL, cnt[q] / 2) : 0;
-        sum += ecnt[q];
+        lo_sum += cnt[q] >= 2 ? 1 : 0;
+        hi_sum += cnt[q] >= 2 ? cnt[q] - 1 : cnt[q];
       }
-      for (int q = 0; sum < need && q < 4 * pairs; ++q) {  // raise E counts up to cnt - 1
-        const int i = q % pairs;
-        const long long cap = cnt[i] >= 2 ? cnt[i] - 1 : cnt[i];
-        if (ecnt[i] < cap) ++ecnt[i], ++sum;
+      skew = false;
+      for (long long dm = 0; dm <= mbk && !skew; ++dm)
+        for (long long cand : {mbk / 2 - dm, (mbk + 1) / 2 + dm})
+          if (!skew && cand >= 1 && cand < mbk && cand * tpm >= lo_sum && cand * tpm <= hi_sum) {
+            mbE = cand;
+            skew = true;
+          }
+      if (skew) {
+        long long need = mbE * tpm, sum = 0;
+        for (int q = 0; q < pairs; ++q) {
+          ecnt[q] = cnt[q] >= 2 ? std::max(1LL, cnt[q] / 2) : 0;
+          sum += ecnt[q];
+        }
+        for (int q = 0; sum < need && q < 4 * pairs; ++q) {  // raise E counts up to cnt - 1
+          const int i = q % pairs;
+          const long long cap = cnt[i] >= 2 ? cnt[i] - 1 : cnt[i];
+          if (ecnt[i] < cap) ++ecnt[i], ++sum;
+        }
+        for (int q = 0; sum > need && q < 4 * pairs; ++q) {  // lower them down to 1 (0 for single tiles)
+          const int i = pairs - 1 - q % pairs;
+          const long long floor_ = cnt[i] >= 2 ? 1 : 0;
+          if (ecnt[i] > floor_) --ecnt[i], --sum;
+        }
+        skew = sum == need;
       }
-      for (int q = 0; sum > need && q < 4 * pairs; ++q) {  // lower them down to 1 (0 for single tiles)
-        const int i = pairs - 1 - q % pairs;
-        const long long floor_ = cnt[i] >= 2 ? 1 : 0;
-        if (ecnt[i] > floor_) --ecnt[i], --sum;
+    }
+    if (skew) {
+      long long je = 0, jl = mbE * tpm;  // cursors into the m-major list (E blocks first)
+      for (int q = 0; q < pairs; ++q) {
+        goff[q] = (int)tiles.size();
+        for (long long k = 0; k < ecnt[q]; ++k) tiles.push_back(mmaj[je++]);
+        for (long long k = ecnt[q]; k < cnt[q]; ++k) tiles.push_back(mmaj[jl++]);
       }
-      skew = sum == need;
+    } else if (order == "block") {
+      // m-major list dealt round-robin: at position j the pairs hold whole replica
+      // blocks (~pairs / tiles-per-block of them), so block m's sweep-t tiles all
+      // finish at one position and its sweep-(t+1) tiles run a full sweep later
+      for (int q = 0; q < pairs; ++q) {
+        goff[q] = (int)tiles.size();
+        for (long long j = q; j < T; j += pairs) tiles.push_back(mmaj[j]);
+      }
+    } else if (order == "spin") {
+      std::vector<DenseTile> sorted(mmaj);
+      std::stable_sort(sorted.begin(), sorted.end(),
+                       [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
+      for (int q = 0; q < pairs; ++q) {
+        goff[q] = (int)tiles.size();
+        for (long long j = q; j < T; j += pairs) tiles.push_back(sorted[j]);
+      }
+    } else {
+      for (int q = 0; q < pairs; ++q) {
+        goff[q] = (int)tiles.size();
+        const long long j0 = T * q / pairs, j1 = T * (q + 1) / pairs;
+        std::vector<DenseTile> run(mmaj.begin() + j0, mmaj.begin() + j1);
+        if (order == "sorted")
+          std::stable_sort(run.begin(), run.end(),
+                           [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
+        if ((order == "alt" && (q & 1)) || order == "rev") std::reverse(run.begin(), run.end());
+        tiles.insert(tiles.end(), run.begin(), run.end());
+      }
     }
-  }
-  if (skew) {
-    long long je = 0, jl = mbE * tpm;  // cursors into the m-major list (E blocks first)
-    for (int q = 0; q < pairs; ++q) {
-      off[q] = (int)tiles.size();
-      for (long long k = 0; k < ecnt[q]; ++k) tiles.push_back(mmaj[je++]);
-      for (long long k = ecnt[q]; k < cnt[q]; ++k) tiles.push_back(mmaj[jl++]);
-    }
-  } else if (order == "block") {
-    // m-major list dealt round-robin: at position j the pairs hold whole replica
-    // blocks (~pairs / tiles-per-block of them), so block m's sweep-t tiles all
-    // finish at one position and its sweep-(t+1) tiles run a full sweep later
-    for (int q = 0; q < pairs; ++q) {
-      off[q] = (int)tiles.size();
-      for (long long j = q; j < T; j += pairs) tiles.push_back(mmaj[j]);
-    }
-  } else if (order == "spin") {
-    std::vector<DenseTile> sorted(mmaj);
-    std::stable_sort(sorted.begin(), sorted.end(),
-                     [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
-    for (int q = 0; q < pairs; ++q) {
-      off[q] = (int)tiles.size();
-      for (long long j = q; j < T; j += pairs) tiles.push_back(sorted[j]);
-    }
-  } else {
-    for (int q = 0; q < pairs; ++q) {
-      off[q] = (int)tiles.size();
-      const long long j0 = T * q / pairs, j1 = T * (q + 1) / pairs;
-      std::vector<DenseTile> run(mmaj.begin() + j0, mmaj.begin() + j1);
-      if (order == "sorted")
-        std::stable_sort(run.begin(), run.end(),
-                         [](const DenseTile& x, const DenseTile& y) { return x.n0 < y.n0; });
-      if ((order == "alt" && (q & 1)) || order == "rev") std::reverse(run.begin(), run.end());
-      tiles.insert(tiles.end(), run.begin(), run.end());
-    }
-  }
-  off[pairs] = (int)tiles.size();
+    goff[pairs] = (int)tiles.size();
+    off.insert(off.end(), goff.begin(), goff.end());
+  }  // groups
+  if (getenv("NMFA_DENSE_VERBOSE"))
+    fprintf(stderr, "dense plan: Rp=%d groups=%lld w=%d tiles=%zu footprint/group=%.1f MB\n",
+            ds->Rp, n_groups, best_w, tiles.size(), footprint(mb_g) / 1e6);
+  // widest launch (sizes the debug traces; NMFA_TRACE2 decodes group 0 only)
+  ds->pairs = *std::max_element(ds->grp_pairs.begin(), ds->grp_pairs.end());
+  const long long T = (long long)tiles.size();
   // K order per tile: natural (slice 0 first), so a spin's fp32 field is summed
   // in the same order for every schedule, replica count and row sharding.  The
   // debug knob NMFA_KORDER=early consumes slices earliest-published first
@@ -1155,12 +1196,15 @@ int dense_plan_alloc(nmfa_plan* pl) {
   const std::string kord_s = korder_env ? korder_env : "";
   const bool rotate = kord_s == "rotate" || kord_s == "rotm" || kord_s == "rotmn";
   std::vector<int> avail((size_t)mb * kbn, 0);
-  for (int q = 0; q < pairs; ++q)
-    for (int j = off[q]; j < off[q + 1]; ++j) {
-      const DenseTile& t = tiles[j];
-      for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb)
-        avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - off[q]);
-    }
+  for (size_t g = 0; g < ds->grp_pairs.size(); ++g) {
+    const int* go = off.data() + ds->grp_off_base[g];
+    for (int q = 0; q < ds->grp_pairs[g]; ++q)
+      for (int j = go[q]; j < go[q + 1]; ++j) {
+        const DenseTile& t = tiles[j];
+        for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb)
+          avail[(size_t)t.m_blk * kbn + kb] = std::max(avail[(size_t)t.m_blk * kbn + kb], j - go[q]);
+      }
+  }
   std::vector<int16_t> korder;
   if (early || rotate) korder.resize((size_t)T * kbn);
   for (long long j = 0; j < T; ++j) {
@@ -1199,13 +1243,10 @@ int dense_plan_alloc(nmfa_plan* pl) {
   // Readiness is counted per (replica block, k-slice) in spin-quarters; slices
   // of other shards need 0.
   std::vector<unsigned> kneed((size_t)mb * kbn, 0);
-  for (int q = 0; q < pairs; ++q)
-    for (int j = off[q]; j < off[q + 1]; ++j) {
-      const DenseTile& t = tiles[j];
-      for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb) {
-        const int lo_s = std::max(t.n0, kb * 128), hi_s = std::min(t.n0 + t.nlen, kb * 128 + 128);
-        kneed[(size_t)t.m_blk * kbn + kb] += 8u * (unsigned)(hi_s - lo_s);  // 2 CTAs x 4 quarters
-      }
+  for (const DenseTile& t : tiles)
+    for (int kb = t.n0 >> 7; kb <= (t.n0 + t.nlen - 1) >> 7; ++kb) {
+      const int lo_s = std::max(t.n0, kb * 128), hi_s = std::min(t.n0 + t.nlen, kb * 128 + 128);
+      kneed[(size_t)t.m_blk * kbn + kb] += 8u * (unsigned)(hi_s - lo_s);  // 2 CTAs x 4 quarters
     }
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_kneed, kneed.size() * sizeof(unsigned)));
   NMFA_CUDA_TRY(cudaMemcpy(ds->d_kneed, kneed.data(), kneed.size() * sizeof(unsigned),
@@ -1346,7 +1387,14 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
     a.peer0[k] = ds->peer_img[0][k];
     a.peer1[k] = ds->peer_img[1][k];
   }
-  NMFA_CUDA_TRY(cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1], a));
+  // one persistent launch per replica group (L2-aware split, dense_plan_alloc)
+  for (size_t g = 0; g < ds->grp_pairs.size(); ++g) {
+    a.tile_off = ds->d_tile_off + ds->grp_off_base[g];
+    cfgl.gridDim = dim3(2 * ds->grp_pairs[g]);
+    NMFA_CUDA_TRY(
+        cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1], a));
+  }
+  launches += (int64_t)ds->grp_pairs.size() - 1;
   add_launches(launches);
   if (tl3_path) {
     cudaStreamSynchronize(st);
