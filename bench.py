@@ -132,7 +132,11 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def load_traffic(workload):
+def load_traffic(workload, reads_override=None):
+    """ncu DRAM bytes of one launch of the workload's default shape
+    (profiles/ncu_summary.json); null when --reads changes the shape."""
+    if reads_override is not None:
+        return None
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
@@ -668,7 +672,7 @@ def run_ours(args):
         achieved = flop / per_launch_s / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.workload),
+                "frac": achieved / peak, "traffic": load_traffic(args.workload, args.reads),
                 "kernel": f"{info['path']} NMFA anneal (tcgen05, fused epilogue; one launch = t_f sweeps "
                           "+ exact energies)",
                 "algorithmic_per_launch": f"2*N^2*R*t_f = {flop * t_f:.4g} FLOP (N={n}, R={R}, "
@@ -691,7 +695,7 @@ def run_ours(args):
         achieved = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.workload),
+                "frac": achieved / peak, "traffic": load_traffic(args.workload, args.reads),
                 "timing": "CUDA events around the anneal launches inside the timed, L2-flushed steps",
                 "kernel": ("sparse NMFA step (ELL gather, %d slots per row, fused epilogue)" % info["ell_slots"]
                            if info.get("ell_slots") else "sparse NMFA step (CSR gather, fused epilogue)"),
