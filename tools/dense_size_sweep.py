@@ -10,11 +10,14 @@ import torch  # noqa: E402
 import paper_1806_08422_b200 as nb  # noqa: E402
 
 PEAK = 1363.6  # MEASURED_PEAKS bf16 sustained TFLOP/s
-t_f = 100
-for n in (1000, 2000, 4000, 8000):
+# optional: tools/dense_size_sweep.py N1,N2,.. R1,R2,.. t_f
+NS = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else (1000, 2000, 4000, 8000)
+RS = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else (4096, 8192, 16384)
+t_f = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+for n in NS:
     p = nb.gen_sk(n, 3)
     p.device_handle().set_path("dense")
-    for R in (4096, 8192, 16384):
+    for R in RS:
         params = nb.NmfaParams(t_f=t_f, seed=0)
         plan = nb.Plan(p, R, params.schedule.temperatures(t_f), params.alpha, params.sigma)
         cfg = torch.empty((R, n), dtype=torch.int8, device="cuda")
