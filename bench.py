@@ -55,6 +55,7 @@ WORKLOADS = {
 
 DTYPES = {
     "dense": "f16 operand / f16 hi+lo state (~22-bit) / f32 accumulate",
+    "dense_hilo": "f16 hi+lo operands (HILO field, ~22-bit) / f16 hi+lo state / f32 accumulate",
     "small": "f16 operand / f32 state / f32 accumulate",
     "sparse": "f32 state / f32 accumulate",
 }
@@ -601,6 +602,8 @@ def run_ours(args):
     if args.reads:
         R = args.reads
     p = build_problem(nb, args.workload)
+    if args.field != "fp16":
+        p.device_handle(local).set_field_precision(args.field)
     params = nb.NmfaParams(t_f=t_f, seed=args.seed)
     temps = params.schedule.temperatures(t_f)
     plan = nb.Plan(p, R, temps, params.alpha, params.sigma, device=local)
@@ -772,10 +775,14 @@ def run_ours(args):
             "metric": metric_name(args.workload), "value": value,
             "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[info["path"]],
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": DTYPES["dense_hilo"] if info.get("field") == "hilo" and info["path"] == "dense"
+            else DTYPES[info["path"]],
             "data": f"synthetic (reference generator stream, {WORKLOADS[args.workload][0]})",
             "config": {"workload": desc, "reads_per_gpu": R, "reads_total": R * world,
                        "n": n, "t_f": t_f, "path": info["path"],
+                       **({"field": "hilo (2 MMAs per k-slice; roofline counts the algorithmic "
+                                    "2 N^2 R FLOP per sweep)"} if args.field == "hilo" else {}),
                        "parallelism": f"replica-sharded x{world}",
                        "l2": "flushed between timed steps (256 MB write outside the per-step "
                              "event brackets); value = steps x work / sum of step times",
@@ -813,6 +820,9 @@ def main():
     ap.add_argument("--no-tts", action="store_true", help="skip the SK100 TTS99 side measurement")
     ap.add_argument("--no-stats", action="store_true",
                     help="skip the success-probability side measurements (SK100, Moebius-100, G2000)")
+    ap.add_argument("--field", choices=["fp16", "hilo"], default="fp16",
+                    help="dense path GEMM operand: fp16 hi (default, the throughput mode) or the "
+                         "HILO fidelity mode (hi + lo; NMFA_FIELD_HILO)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="nccl",
                     help="sk65536: NCCL all-gather per sweep (default) or the fused peer-store "
                          "exchange (p2p; falls back to NCCL when symmetric memory is unavailable)")

@@ -38,6 +38,17 @@ extern "C" {
 #define NMFA_PATH_DENSE 1  /* dense n > 256: tcgen05 GEMM step, J streamed */
 #define NMFA_PATH_SPARSE 2 /* sparse n > 256: ELL (max degree <= 4) or CSR gather step */
 
+/* Precision of the dense path's GEMM operand (the field J.s; the state itself is
+ * always fp16 hi + fp16 lo, ~22 bits).  FP16: the hi part only (one tcgen05 MMA
+ * per k-slice; the throughput mode, trajectories within 2e-3 of float64).  HILO:
+ * hi and lo both enter the GEMM (two MMAs per k-slice into one fp32
+ * accumulator, a second lo image; about half the throughput), so the field
+ * carries the full state and trajectories follow the float64 reference like
+ * the fp32 sparse path (the fidelity mode).  The small path
+ * (n <= 256) has fp16 operands only; the sparse path is fp32 either way. */
+#define NMFA_FIELD_FP16 0
+#define NMFA_FIELD_HILO 1
+
 typedef struct nmfa_problem nmfa_problem_t;
 typedef struct nmfa_plan nmfa_plan_t;
 
@@ -52,7 +63,7 @@ typedef struct {
   double j_scale;      /* power-of-two scale applied to J on device */
   int32_t ell_slots;   /* sparse path: ELL row length (3 or 4) when the max
                           degree is <= 4, 0 when rows use the CSR kernel */
-  int32_t reserved;
+  int32_t field;       /* NMFA_FIELD_* (nmfa_problem_set_field_precision) */
 } nmfa_problem_info_t;
 
 /* Build an immutable device-resident problem from the canonical coupler
@@ -112,6 +123,14 @@ int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int6
 /* Force a kernel path (tests / crossover studies); NMFA_ERR_ARG if the path
  * cannot run this problem (e.g. SMALL with n > 256). */
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path);
+
+/* Dense-path operand precision for plans created from now on (NMFA_FIELD_*;
+ * default FP16).  Drops the problem's cached plan; existing explicit plans keep
+ * the precision they were built with.  NMFA_ERR_ARG for HILO on a problem whose
+ * path is SMALL, and for a row shard (its exchange carries the hi image only).
+ * No reference counterpart: the reference computes the field in float64
+ * (_kernels_numba.py:72); HILO is the closest this path gets to it. */
+int nmfa_problem_set_field_precision(nmfa_problem_t* p, int32_t field);
 
 /* A plan owns the device state for `n_reads` replicas and `t_f` steps so
  * repeated runs allocate nothing and can be captured in a CUDA graph.  A plan

@@ -20,6 +20,8 @@ LIB_PATH = os.path.join(_HERE, "libnmfa_b200_guard.so" if os.environ.get("NMFA_L
 NMFA_OK, NMFA_ERR_ARG, NMFA_ERR_CUDA, NMFA_ERR_STATE = 0, 1, 2, 3
 PATH_SMALL, PATH_DENSE, PATH_SPARSE = 0, 1, 2
 PATH_NAMES = {PATH_SMALL: "small", PATH_DENSE: "dense", PATH_SPARSE: "sparse"}
+# dense-path GEMM operand precision (NMFA_FIELD_*, include/nmfa_b200.h)
+FIELD_NAMES = {0: "fp16", 1: "hilo"}
 
 # Every symbol include/nmfa_b200.h declares: name -> (restype, argtypes)
 _p, _i32, _i64, _u64, _f64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
@@ -33,6 +35,7 @@ SIGNATURES = {
     "nmfa_problem_create_csr": (_i32, [_i64, _p, _p, _p, _p, _i32, ctypes.POINTER(_p)]),
     "nmfa_problem_get_info": (_i32, [_p, _p]),
     "nmfa_problem_set_path": (_i32, [_p, _i32]),
+    "nmfa_problem_set_field_precision": (_i32, [_p, _i32]),
     "nmfa_plan_create": (_i32, [_p, _i64, _i32, _p, _f64, _f64, ctypes.POINTER(_p)]),
     "nmfa_plan_destroy": (_i32, [_p]),
     "nmfa_plan_run": (_i32, [_p, _u64, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
@@ -64,7 +67,7 @@ SIGNATURES = {
 class ProblemInfo(ctypes.Structure):
     _fields_ = [("n", _i64), ("n_edges", _i64), ("density", _f64), ("is_dense", _i32),
                 ("path", _i32), ("j_exact", _i32), ("int_weights", _i32), ("j_scale", _f64),
-                ("ell_slots", _i32), ("reserved", _i32)]
+                ("ell_slots", _i32), ("field", _i32)]
 
 
 _lib = None

@@ -28,6 +28,13 @@
 // of exactly the tile half, <= 32 KB), 2 TMEM accumulator slots of 256
 // columns so the epilogue of tile j overlaps the MMAs of tile j+1.
 //
+// Field precision (NMFA_FIELD_*): FP16 multiplies the hi part of the state
+// (one MMA per k-slice).  HILO multiplies hi and then lo for every k-slice into
+// the same fp32 accumulator (two ring stages per k-slice, B loaded for each),
+// so the field sees the full ~22-bit state; lo then ping-pongs between two
+// images like hi, because other tiles' GEMMs read it while its owner rewrites
+// it.  The energy pass multiplies the +-1 configuration (hi) alone.
+//
 // Persistence: one cooperative launch runs every sweep of the anneal (plus the
 // exact energy pass).  Each pair owns 3-4 (replica block, spin range) tiles
 // per sweep in a skewed order: the replica blocks are split into an early and
@@ -111,6 +118,8 @@ struct DenseState {
   long long Rp = 0;
   long long slice_b = 0;           // bytes per k-slice of an operand image (Rp * 256 + pad)
   uint8_t* lo_img = nullptr;
+  uint8_t* lo_img2 = nullptr;      // HILO field: second lo image (lo ping-pongs like hi)
+  bool hilo = false;               // NMFA_FIELD_HILO: hi and lo both enter the GEMM
   uint8_t* a_img[2] = {nullptr, nullptr};
   DenseTile* d_tiles = nullptr;
   int* d_tile_off = nullptr;
@@ -122,6 +131,7 @@ struct DenseState {
   std::vector<int> grp_pairs;     // per replica group: CTA pairs of its launch
   int16_t* d_korder = nullptr;     // [tile][kblocks] K order (null: natural)
   CUtensorMap tmA[2];
+  CUtensorMap tmL[2];  // lo images as A operands (HILO field; copies of tmA otherwise)
   CUtensorMap tmB[2];  // B boxes of exactly one tile half (2 x rows lines), the two widths
   int bhalf[2] = {0, 0};
   // fused exchange (row-sharded J): the operand images are peer-accessible
@@ -149,7 +159,9 @@ struct DenseStepArgs {
   const float* hn;
   uint8_t* img0;           // operand images (hi part of the state), ping-pong by parity
   uint8_t* img1;
-  uint8_t* lo;             // residual image, same layout
+  uint8_t* lo;             // residual image, same layout (HILO: lo of even sweeps)
+  uint8_t* lo1;            // HILO: lo of odd sweeps (the GEMM reads lo, so it ping-pongs)
+  int hilo;                // HILO field: A = hi then lo per k-slice, one fp32 accumulator
   unsigned long long key_base;
   const float* noise;
   int8_t* cfg;
@@ -331,7 +343,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     dense_anneal_kernel(const __grid_constant__ CUtensorMap tmA0,
                         const __grid_constant__ CUtensorMap tmA1,
                         const __grid_constant__ CUtensorMap tmB0,
-                        const __grid_constant__ CUtensorMap tmB1, const DenseStepArgs a) {
+                        const __grid_constant__ CUtensorMap tmB1,
+                        const __grid_constant__ CUtensorMap tmL0,
+                        const __grid_constant__ CUtensorMap tmL1, const DenseStepArgs a) {
   extern __shared__ __align__(1024) uint8_t dsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -348,9 +362,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
   const int n_phases = (a.t_end - a.t_begin) + (a.energy_pass ? 1 : 0);
 
   if (warp == kWarpProducer && lane == 0) {
-    const CUtensorMap* maps[4] = {&tmA0, &tmA1, &tmB0, &tmB1};
+    const CUtensorMap* maps[6] = {&tmA0, &tmA1, &tmB0, &tmB1, &tmL0, &tmL1};
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < (a.hilo ? 6 : 4); ++m)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(maps[m])) : "memory");
     for (int s = 0; s < kDStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -378,6 +392,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       for (int ph = 0; ph < n_phases; ++ph) {
         const int t = a.t_begin + ph;
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
+        const CUtensorMap* tmL = (t & 1) ? &tmL1 : &tmL0;
+        // HILO field: every k-slice is two stages, A = hi then A = lo (same B);
+        // the energy pass multiplies the +-1 configuration (hi) only
+        const int subs = (a.hilo && t < a.t_end) ? 2 : 1;
         for (int j = j0; j < j1; ++j) {
           const DenseTile tl = a.tiles[j];
           const int half = tl.nlen >> 1;
@@ -390,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           if (t2) t2[0] = gtimer();
           long long wempty = 0;
           const unsigned long long step = (unsigned long long)jglob << 16;
-          for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
+          for (int ki = 0; ki < a.kblocks; ++ki) {
             const int kb = kord ? kord[ki] : ki;
             if (seen < step + (unsigned long long)(ki + 1)) {
               // the slices of block m for sweep t were written by sweep t-1: the
@@ -407,40 +425,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               a.trace[jglob * 8 + 1] = clock64();  // producer reached the last slice
             if (t2 && ki == 0) t2[5] = gtimer();
             if (t2 && ki == a.kblocks - 1) t2[1] = gtimer();
-            const int s = it % kDStages;
-            NMFA_JITTER(blockIdx.x, it);  // checked build only
-            if (a.trace) {
-              const long long c0 = clock64();
-              mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
-              wempty += clock64() - c0;
-            } else {
-              mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
-            }
-            if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 0] = clock64();
-            const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
-            if (cta == 0)
+            for (int sub = 0; sub < subs; ++sub, ++it) {
+              const int s = it % kDStages;
+              NMFA_JITTER(blockIdx.x, it);  // checked build only
+              if (a.trace) {
+                const long long c0 = clock64();
+                mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+                wempty += clock64() - c0;
+              } else {
+                mbar_wait(&empty_bar[s], ((it / kDStages) & 1) ^ 1);
+              }
+              if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 0] = clock64();
+              const uint32_t fb = map_to_rank(smem_u32(&full_bar[s]), 0);
+              if (cta == 0)
 #ifdef NMFA_DBG_NOB  // timing bound only: no J bytes through TMA (results are wrong)
-              mbar_arrive_expect_tx(&full_bar[s], 2u * kATile);
+                mbar_arrive_expect_tx(&full_bar[s], 2u * kATile);
 #else
-              mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
+                mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
 #endif
-            uint8_t* st = smem + (size_t)s * kDStageBytes;
-            tma2d_pair(smem_u32(st), tmA, 0, (int)(kb * (a.slice_b >> 7) + arow * 2), fb, pol_keep);
+              uint8_t* st = smem + (size_t)s * kDStageBytes;
+              tma2d_pair(smem_u32(st), sub ? tmL : tmA, 0, (int)(kb * (a.slice_b >> 7) + arow * 2), fb,
+                         pol_keep);
 #ifndef NMFA_DBG_NOB
-            // J rows of this CTA's half of the tile: ONE box (the per-box TMA cost is
-            // ~100 cycles, so the half is never split into power-of-two boxes)
-            tma2d_pair(smem_u32(st + kATile), half == a.bhalf1 ? &tmB1 : &tmB0, 0,
-                       (kb * a.brows + brow) * 2, fb, pol_keep);
+              // J rows of this CTA's half of the tile: ONE box (the per-box TMA cost is
+              // ~100 cycles, so the half is never split into power-of-two boxes)
+              tma2d_pair(smem_u32(st + kATile), half == a.bhalf1 ? &tmB1 : &tmB0, 0,
+                         (kb * a.brows + brow) * 2, fb, pol_keep);
 #endif
 #ifdef NMFA_L2_PREFETCH  // experiment: pull the A box NMFA_L2_PREFETCH k-slices ahead into L2
-            if (ki + NMFA_L2_PREFETCH < a.kblocks) {
-              const int kb2 = kord ? kord[ki + NMFA_L2_PREFETCH] : ki + NMFA_L2_PREFETCH;
-              asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                               reinterpret_cast<uint64_t>(tmA)),
-                           "r"(0), "r"((int)(kb2 * (a.slice_b >> 7) + arow * 2))
-                           : "memory");
-            }
+              if (ki + NMFA_L2_PREFETCH < a.kblocks) {
+                const int kb2 = kord ? kord[ki + NMFA_L2_PREFETCH] : ki + NMFA_L2_PREFETCH;
+                asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                                 reinterpret_cast<uint64_t>(tmA)),
+                             "r"(0), "r"((int)(kb2 * (a.slice_b >> 7) + arow * 2))
+                             : "memory");
+              }
 #endif
+            }  // sub
           }
           if (a.trace && blockIdx.x == 0 && jglob < 512)
             a.trace[jglob * 8 + 7] = wempty;  // cycles the producer waited for a free stage
@@ -454,6 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const uint64_t desc0 = make_desc_noswizzle(smem_u32(smem), 128, 2048);
       const uint32_t desc_lo0 = (uint32_t)desc0, desc_hi = (uint32_t)(desc0 >> 32);
       for (int ph = 0; ph < n_phases; ++ph) {
+        const int subs = (a.hilo && a.t_begin + ph < a.t_end) ? 2 : 1;  // as the producer
         for (int j = j0; j < j1; ++j, ++jj) {
           const DenseTile tl = a.tiles[j];
           const int slot = jj & 1, use = jj >> 1;
@@ -464,7 +486,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
           const uint32_t idesc = make_idesc_f16(256, (uint32_t)tl.nlen);
           const uint32_t d = tbase + (uint32_t)slot * kAccCols;
           long long wfull = 0;
-          for (int ki = 0; ki < a.kblocks; ++ki, ++it) {
+          for (int ki = 0; ki < a.kblocks; ++ki)
+          for (int sub = 0; sub < subs; ++sub, ++it) {
             const int s = it % kDStages;
             NMFA_JITTER(blockIdx.x + 7919, it);  // checked build only
             if (a.trace) {
@@ -481,10 +504,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             if (ki != tl.pad) {
 #pragma unroll
               for (int ks = 0; ks < kBK / 16; ++ks)
-                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | ks) ? 1u : 0u);
+                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | sub | ks) ? 1u : 0u);
             } else {
               for (int ks = 0; ks < a.k_last_sub; ++ks)
-                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | ks) ? 1u : 0u);
+                mma_pair(d, a_lo + ks * 16, b_lo + ks * 16, desc_hi, idesc, (ki | sub | ks) ? 1u : 0u);
             }
             commit_pair_mc(&empty_bar[s]);
             if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 2] = clock64();
@@ -555,10 +578,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     const float4* invn4 = reinterpret_cast<const float4*>(a.invn);
     const float4* hn4 = reinterpret_cast<const float4*>(a.hn);
     #ifdef NMFA_DBG_LOKEEP  // experiment: keep the lo residual in L2 too
-    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_last();
+    const uint64_t pol_keep = policy_evict_last(), pol_stream0 = policy_evict_last();
 #else
-    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last(), pol_stream0 = policy_evict_first();
 #endif
+    // HILO: lo is a GEMM operand re-read by every pair of its block, like hi
+    const uint64_t pol_stream = a.hilo ? pol_keep : pol_stream0;
     int jj = 0;
     for (int ph = 0; ph < n_phases; ++ph) {
       const int t = a.t_begin + ph;
@@ -567,6 +592,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
       const float inv_t = energy_phase ? 0.f : __ldg(a.inv_temp + t);
       const uint8_t* a_cur = (t & 1) ? a.img1 : a.img0;
       uint8_t* a_next = (t & 1) ? a.img0 : a.img1;
+      // lo is read and rewritten in place by its owning tile alone, unless the
+      // GEMM reads it too (HILO): then it ping-pongs with the sweep parity
+      const uint8_t* lo_cur = (a.hilo && (t & 1)) ? a.lo1 : a.lo;
+      uint8_t* lo_next = (a.hilo && !(t & 1)) ? a.lo1 : a.lo;
       for (int j = j0; j < j1; ++j, ++jj) {
         const DenseTile tl = a.tiles[j];
         const int slot = jj & 1, use = jj >> 1;
@@ -623,11 +652,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             if (c < c_hi) {
               const long long off = img_off(tl.n0 + c);
               asm volatile("prefetch.global.L1 [%0];" ::"l"(a_cur + off));
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.lo + off));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(lo_cur + off));
               if (c + 8 < c_hi) {
                 const long long off2 = img_off(tl.n0 + c + 8);
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(a_cur + off2));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.lo + off2));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(lo_cur + off2));
               }
             }
 #endif
@@ -664,9 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               for (int q = 0; q < 8; ++q) lo[8 * h + q] = 0.f;
 #elif !defined(NMFA_DBG_NOMEM) && defined(NMFA_HILO_PLAIN)  // A/B: two converts + FADD
               unpack_half8(ld_hint(a_cur + off, pol_keep), ms + 8 * h);
-              unpack_half8(ld_hint(a.lo + off, pol_stream), lo + 8 * h);
+              unpack_half8(ld_hint(lo_cur + off, pol_stream), lo + 8 * h);
 #elif !defined(NMFA_DBG_NOMEM)
-              hilo_sum8(ld_hint(a_cur + off, pol_keep), ld_hint(a.lo + off, pol_stream), ms + 8 * h);
+              hilo_sum8(ld_hint(a_cur + off, pol_keep), ld_hint(lo_cur + off, pol_stream), ms + 8 * h);
 #pragma unroll
               for (int q = 0; q < 8; ++q) lo[8 * h + q] = -0.f;  // x + (-0) == x for every x
 #else
@@ -700,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               if (lv.x == 0x12345u && lv.y == 7u) a.lo[0] = 1;
 #elif !defined(NMFA_DBG_NOMEM)
               st_hint(a_next + off, hv, pol_keep);
-              st_hint(a.lo + off, lv, pol_stream);
+              st_hint(lo_next + off, lv, pol_stream);
               // fused exchange: the same 16 bytes into every other shard's image
               // (NVLink peer stores, overlapped with the GEMM of the next tile)
               for (int pk = 0; pk < a.n_peers; ++pk)
@@ -972,6 +1001,7 @@ void dense_plan_free(nmfa_plan* pl) {
   auto* ds = static_cast<DenseState*>(pl->dense);
   if (!ds) return;
   if (ds->lo_img) cudaFree(ds->lo_img);
+  if (ds->lo_img2) cudaFree(ds->lo_img2);
   if (!ds->external_images) {
     if (ds->a_img[0]) cudaFree(ds->a_img[0]);
     if (ds->a_img[1]) cudaFree(ds->a_img[1]);
@@ -1010,6 +1040,17 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(cudaMalloc(&ds->a_img[1], img_bytes));
   NMFA_CUDA_TRY(cudaMemset(ds->a_img[0], 0, img_bytes));
   NMFA_CUDA_TRY(cudaMemset(ds->a_img[1], 0, img_bytes));
+  ds->hilo = pl->field == NMFA_FIELD_HILO;
+  if (ds->hilo) {
+    if (dense_is_sharded(p)) {
+      set_error("field precision HILO is not available on a row shard");
+      return NMFA_ERR_ARG;
+    }
+    // the GEMM reads lo over the whole padded k range: zero it once (the
+    // epilogue never writes spins >= the padded n, and J is zero there)
+    NMFA_CUDA_TRY(cudaMalloc(&ds->lo_img2, img_bytes));
+    NMFA_CUDA_TRY(cudaMemset(ds->lo_img2, 0, img_bytes));
+  }
 
   // Static schedule.  A tile is (replica block of 256, w x 16 spins); per
   // k-slice of 128 it costs max(MMA = 64 w, TMA = 563 + 22.6 w) cycles
@@ -1034,7 +1075,8 @@ int dense_plan_alloc(nmfa_plan* pl) {
   // across devices and stay one group.  NMFA_DENSE_GROUPS=k forces k groups,
   // NMFA_L2_BUDGET_MB sets the budget.
   const double j_bytes = (double)ds->kp * p->brows * 2.0;
-  auto footprint = [&](long long blocks) { return 3.0 * 2.0 * ds->kp * 256.0 * blocks + j_bytes; };
+  const double images = ds->hilo ? 4.0 : 3.0;  // two hi images + lo (+ the second lo of HILO)
+  auto footprint = [&](long long blocks) { return images * 2.0 * ds->kp * 256.0 * blocks + j_bytes; };
   static const char* budget_env = getenv("NMFA_L2_BUDGET_MB");
   const double budget = (budget_env ? atof(budget_env) : 120.0) * 1e6;
   const long long tpm_est = (upm + 13) / 14;
@@ -1254,9 +1296,14 @@ int dense_plan_alloc(nmfa_plan* pl) {
   NMFA_CUDA_TRY(cudaMalloc(&ds->d_ready, kneed.size() * sizeof(unsigned)));
 
   int err;
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 2; ++b) {
     if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * (ds->slice_b >> 7), 256)))
       return err;
+    ds->tmL[b] = ds->tmA[b];
+    if (ds->hilo && (err = make_line_map(&ds->tmL[b], b ? ds->lo_img2 : ds->lo_img,
+                                         (uint64_t)ds->kblocks * (ds->slice_b >> 7), 256)))
+      return err;
+  }
   // one B tensor map per distinct tile width (balanced widths: at most two)
   {
     int hs[2] = {-1, -1}, nh = 0;
@@ -1338,6 +1385,8 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   a.img0 = ds->a_img[0];
   a.img1 = ds->a_img[1];
   a.lo = ds->lo_img;
+  a.lo1 = ds->lo_img2;
+  a.hilo = ds->hilo ? 1 : 0;
   a.key_base = key_base;
   a.noise = noise;
   a.cfg = cfg;
@@ -1392,7 +1441,8 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
     a.tile_off = ds->d_tile_off + ds->grp_off_base[g];
     cfgl.gridDim = dim3(2 * ds->grp_pairs[g]);
     NMFA_CUDA_TRY(
-        cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1], a));
+        cudaLaunchKernelEx(&cfgl, kern, ds->tmA[0], ds->tmA[1], ds->tmB[0], ds->tmB[1],
+                           ds->tmL[0], ds->tmL[1], a));
   }
   launches += (int64_t)ds->grp_pairs.size() - 1;
   add_launches(launches);
@@ -1466,6 +1516,10 @@ int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int 
       set_error("NULL exchange buffer");
       return NMFA_ERR_ARG;
     }
+  if (ds->hilo) {
+    set_error("the fused exchange carries the hi image only; use an FP16-field plan");
+    return NMFA_ERR_ARG;
+  }
   const bool own = img0[rank] == ds->a_img[0] && img1[rank] == ds->a_img[1];
   if (!own) {  // adopt the caller's buffers (not freed by the plan)
     if (!ds->external_images) {
@@ -1477,9 +1531,11 @@ int dense_set_exchange(nmfa_plan* pl, void* const* img0, void* const* img1, int 
     ds->a_img[1] = static_cast<uint8_t*>(img1[rank]);
   }
   int err;
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 2; ++b) {
     if ((err = make_line_map(&ds->tmA[b], ds->a_img[b], (uint64_t)ds->kblocks * (ds->slice_b >> 7), 256)))
       return err;
+    ds->tmL[b] = ds->tmA[b];  // unused: exchange plans are FP16-field plans
+  }
   ds->n_peers = 0;
   for (int g = 0; g < world; ++g) {
     if (g == rank) continue;

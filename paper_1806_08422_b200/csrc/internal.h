@@ -41,6 +41,7 @@ struct nmfa_problem {
   double density = 0.0;
   bool is_dense = false;   // reference dispatch bit (problem.py:99)
   int32_t path = NMFA_PATH_SPARSE;
+  int32_t field = NMFA_FIELD_FP16;  // dense-path GEMM operand precision (nmfa_problem_set_field_precision)
   bool j_exact = true;
   bool int_weights = true;
   bool has_field = false;  // some h_i != 0 (the energy's field term is skipped otherwise)
@@ -98,6 +99,7 @@ struct nmfa_plan {
   int64_t R = 0;
   int32_t t_f = 0;
   int32_t path = 0;             // the problem's path when the plan was built
+  int32_t field = 0;            // the problem's field precision when the plan was built
   float alpha = 0.f, oma = 0.f, sigma = 0.f;
   float* d_inv_temp = nullptr;  // [t_f]
   std::vector<float> h_inv_temp; // host copy (per-step launches read it)

@@ -198,11 +198,20 @@ class _DeviceProblem:
         return {"n": info.n, "n_edges": info.n_edges, "density": info.density,
                 "is_dense": bool(info.is_dense), "path": _native.PATH_NAMES[info.path],
                 "j_exact": bool(info.j_exact), "int_weights": bool(info.int_weights),
-                "j_scale": info.j_scale, "ell_slots": info.ell_slots}
+                "j_scale": info.j_scale, "ell_slots": info.ell_slots,
+                "field": _native.FIELD_NAMES[info.field]}
 
     def set_path(self, path):
         code = {v: k for k, v in _native.PATH_NAMES.items()}[path]
         _native.check(_native.load().nmfa_problem_set_path(self.handle, code))
+
+    def set_field_precision(self, field):
+        """Dense-path GEMM operand: "fp16" (hi only, the throughput mode) or
+        "hilo" (hi + lo, the fidelity mode); see NMFA_FIELD_* in the header."""
+        codes = {v: k for k, v in _native.FIELD_NAMES.items()}
+        if field not in codes:
+            raise ValueError(f"field precision must be one of {sorted(codes)}, got {field!r}")
+        _native.check(_native.load().nmfa_problem_set_field_precision(self.handle, codes[field]))
 
     def __del__(self):
         try:

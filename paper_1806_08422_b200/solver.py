@@ -258,13 +258,52 @@ class SampleSet:
         return float(be.item()), int(bi.item()) + self.r0
 
 
+class _FieldPrecision:
+    """Use a dense-path field precision ("fp16" / "hilo") for one call and
+    restore the problem's previous setting afterwards (None: leave it)."""
+
+    def __init__(self, problem, device, field):
+        self.dev = problem.device_handle(device) if field is not None else None
+        self.field = field
+
+    def __enter__(self):
+        if self.dev is not None:
+            self.prev = self.dev.info()["field"]
+            if self.prev != self.field:
+                self.dev.set_field_precision(self.field)
+        return self
+
+    def __exit__(self, *exc):
+        if self.dev is not None and self.prev != self.field:
+            self.dev.set_field_precision(self.prev)
+        return False
+
+
+def _replay_field(problem, device, field):
+    """The replay mode is the fidelity mode: on the dense path it multiplies
+    the full hi + lo state (HILO field) unless the caller chose a field."""
+    if field is not None:
+        return field
+    return "hilo" if problem.device_handle(device).info()["path"] == "dense" else None
+
+
 def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=None,
-           temps=None, return_s=False, record_trajectory=False):
+           temps=None, return_s=False, record_trajectory=False, field=None):
     """Run n_runs replicas (global indices r0..r0+n_runs-1) in one device batch.
 
     noise: optional (n_runs, t_f, n) pre-scaled additive noise (device tensor
     or array); when given, params.sigma is unused (run_with_noise seam).
+    field: dense-path GEMM operand for this call, "fp16" or "hilo" (None: the
+    problem's setting, default "fp16"; include/nmfa_b200.h NMFA_FIELD_*).
     """
+    problem = as_problem(problem)
+    with _FieldPrecision(problem, device, field):
+        return _sample(problem, params, n_runs, r0=r0, device=device, noise=noise, s0=s0,
+                       temps=temps, return_s=return_s, record_trajectory=record_trajectory)
+
+
+def _sample(problem, params, n_runs, *, r0, device, noise, s0, temps, return_s,
+            record_trajectory):
     import torch
 
     params = NmfaParams() if params is None else params
@@ -355,7 +394,8 @@ def sample_many(problems, params=None, n_runs=1, *, seeds=None, device=0):
     return cfg, en, time.perf_counter() - t0
 
 
-def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=False, device=0):
+def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=False, device=0,
+                   field=None):
     """Anneal with caller-supplied, pre-scaled noise (solver.py:188-218).
 
     noise (t_f, n) -> returns (s (n,), Trajectory | None), like the reference.
@@ -378,7 +418,7 @@ def run_with_noise(problem, temps, noise, alpha, s0=None, record_trajectory=Fals
         s0 = s0.reshape(R, problem.n)
     params = NmfaParams(alpha=float(alpha), sigma=1.0, t_f=temps.shape[0])
     res = sample(problem, params, R, device=device, noise=nz.astype(np.float32), s0=s0,
-                 temps=temps, return_s=True, record_trajectory=record_trajectory)
+                 temps=temps, return_s=True, record_trajectory=record_trajectory, field=field)
     S = res.s_final.double().cpu().numpy()
     trajs = None
     if record_trajectory:
@@ -395,13 +435,17 @@ def nmfa_step(problem, s, T, params, rng):
 
     The noise comes from the caller's numpy generator, one standard normal per
     spin scaled by sigma, exactly as the reference draws it, so a shared
-    generator gives both packages the same step.
+    generator gives both packages the same step.  On the dense path the step
+    uses the HILO field, as the replay mode does.
     """
     if T <= 0.0:  # the reference's test (a NaN temperature is not rejected there either)
         raise ValueError(f"temperature must be positive, got {T}")
     prob = as_problem(problem)
     drive = params.sigma * rng.standard_normal(prob.n)
-    updated, _ = run_with_noise(prob, np.full(1, float(T)), drive.reshape(1, -1), params.alpha, s0=s)
+    # the reference's own noise, like the replay mode: the same (HILO on the
+    # dense path) field, so t_f steps equal nmfa_run(noise="reference") bitwise
+    updated, _ = run_with_noise(prob, np.full(1, float(T)), drive.reshape(1, -1), params.alpha, s0=s,
+                                field=_replay_field(prob, 0, None))
     return updated
 
 
@@ -446,13 +490,14 @@ def reference_noise(seed, n_runs, t_f, n, sigma, *, r0=0, device=0):
     return out
 
 
-def _replay(problem, params, n_runs, device, record_trajectory):
+def _replay(problem, params, n_runs, device, record_trajectory, field=None):
     """Seeded anneals on the reference's own noise streams: replica chunks of
     at most REPLAY_CHUNK_BYTES of device noise, each generated on the GPU and
     injected through the run_with_noise seam.  One SampleSet for all runs."""
     import torch
 
     problem = as_problem(problem)
+    field = _replay_field(problem, device, field)
     n, t_f = problem.n, int(params.t_f)
     temps = params.schedule.temperatures(t_f)
     chunk = max(1, min(n_runs, REPLAY_CHUNK_BYTES // (4 * t_f * n)))
@@ -461,7 +506,7 @@ def _replay(problem, params, n_runs, device, record_trajectory):
         c = min(chunk, n_runs - c0)
         nz = reference_noise(params.seed, c, t_f, n, params.sigma, r0=c0, device=device)
         res = sample(problem, params, c, device=device, noise=nz, temps=temps,
-                     record_trajectory=record_trajectory)
+                     record_trajectory=record_trajectory, field=field)
         parts.append(res)
         wall += res.wall_clock
         del nz
@@ -476,21 +521,23 @@ def _check_noise_mode(noise):
         raise ValueError(f"noise must be one of {NOISE_MODES}, got {noise!r}")
 
 
-def nmfa_run(problem, params, record_trajectory=False, device=0, noise="device"):
+def nmfa_run(problem, params, record_trajectory=False, device=0, noise="device", field=None):
     """Full anneal from all-zero spins; deterministic given (problem, seed).
 
     noise="reference" replays the reference's own stream for params.seed, so
-    the run follows `nmfa.nmfa_run(problem, params)` step for step."""
+    the run follows `nmfa.nmfa_run(problem, params)` step for step (on the
+    dense path with the HILO field unless `field` says otherwise)."""
     _check_noise_mode(noise)
     if noise == "reference":
-        res = _replay(problem, params, 1, device, record_trajectory)
+        res = _replay(problem, params, 1, device, record_trajectory, field)
     else:
-        res = sample(problem, params, 1, device=device, record_trajectory=record_trajectory)
+        res = sample(problem, params, 1, device=device, record_trajectory=record_trajectory,
+                     field=field)
     return _results(problem, res, params, record_trajectory)[0]
 
 
 def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, device=0,
-               noise="device"):
+               noise="device", field=None):
     """n_runs independent anneals; run k uses seed params.seed + k (solver.py:262-280).
 
     noise="device" (default) draws in-kernel counter-based Philox noise keyed
@@ -498,13 +545,16 @@ def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, devi
     noise="reference" replays each run's own numpy stream noise_stream(seed +
     k) generated on the GPU, so run k is comparable per
     seed with the reference's run k -- slower (the streams are sequential and
-    are injected in replica chunks)."""
+    are injected in replica chunks).  field: the dense path's GEMM operand,
+    "fp16" (hi; the default for device noise) or "hilo" (hi + lo; the default
+    for the replay mode), see sample()."""
     n_runs = int(n_runs)
     if n_runs < 1:
         raise ValueError(f"n_runs must be at least 1, got {n_runs}")
     _check_noise_mode(noise)
     if noise == "reference":
-        res = _replay(problem, params, n_runs, device, record_trajectory)
+        res = _replay(problem, params, n_runs, device, record_trajectory, field)
     else:
-        res = sample(problem, params, n_runs, device=device, record_trajectory=record_trajectory)
+        res = sample(problem, params, n_runs, device=device, record_trajectory=record_trajectory,
+                     field=field)
     return _results(problem, res, params, record_trajectory)

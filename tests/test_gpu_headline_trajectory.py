@@ -23,6 +23,10 @@ on a bifurcation late in the anneal flips a correlated cluster of spins):
 * the GPU tracks its design arithmetic: the dense path's flips are at most
   2x (+2e-4) those of an fp32-state / fp16-operand emulation stepped on the
   same noise here (`_f16_operand_emulation`).
+* dense path with the HILO field (hi + lo state as the GEMM operand, the
+  fidelity mode, include/nmfa_b200.h NMFA_FIELD_HILO): <= 2e-4, 5x inside
+  SURVEY 8(c)'s own 1e-3 (measured 8.6e-5 on K2000, 3.9e-6 on G2000; the
+  remaining gap to float64 is the ~22-bit state and the fp32 sums).
 """
 
 import numpy as np
@@ -82,12 +86,14 @@ def flips(S, Sref):
     return np.mean(np.sign(S) != np.sign(Sref), axis=1)
 
 
-@pytest.mark.parametrize("name,path", [("k2000", "dense"), ("g2000", "dense"), ("g2000", "sparse")])
+@pytest.mark.parametrize("name,path", [("k2000", "dense"), ("g2000", "dense"), ("g2000", "sparse"),
+                                       ("k2000", "dense-hilo"), ("g2000", "dense-hilo")])
 def test_headline_trajectory_matches_float64_reference(name, path):
     op, noise, Sref = reference_run(name)
     q = MAKE[name]()
-    q.device_handle().set_path(path)
-    S, _ = nb.run_with_noise(q, O.temperatures(T_F), noise, SIGMA)
+    q.device_handle().set_path(path.split("-")[0])
+    field = "hilo" if path.endswith("hilo") else None
+    S, _ = nb.run_with_noise(q, O.temperatures(T_F), noise, SIGMA, field=field)
     fl = flips(S, Sref)
     err = np.abs(S - Sref)
     e_gpu = O.energies(op, O.sign_round(S))
@@ -95,8 +101,8 @@ def test_headline_trajectory_matches_float64_reference(name, path):
     print(f"\n{name}/{path}: mean final-sign flips {fl.mean():.2e} (max replica {fl.max():.2e}, "
           f"replicas with any flip {np.mean(fl > 0):.2f}), mean|dS| {err.mean():.2e}; "
           f"identical final energy on {np.mean(e_gpu == e_ref):.2%} of replicas")
-    if path == "sparse":
-        assert fl.mean() <= 1e-4, fl.mean()
+    if path in ("sparse", "dense-hilo"):
+        assert fl.mean() <= (1e-4 if path == "sparse" else 2e-4), fl.mean()
         return
     emu = flips(_f16_operand_emulation(op, noise, O.temperatures(T_F)), Sref)
     print(f"{name}/{path}: fp16-operand emulation on the same noise: mean flips {emu.mean():.2e}")
