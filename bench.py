@@ -56,6 +56,7 @@ WORKLOADS = {
 DTYPES = {
     "dense": "f16 operand / f16 hi+lo state (~22-bit) / f32 accumulate",
     "dense_hilo": "f16 hi+lo operands (HILO field, ~22-bit) / f16 hi+lo state / f32 accumulate",
+    "small_hilo": "f16 hi+lo operands (HILO field, ~22-bit) / f32 state / f32 accumulate",
     "small": "f16 operand / f32 state / f32 accumulate",
     "sparse": "f32 state / f32 accumulate",
 }
@@ -776,8 +777,8 @@ def run_ours(args):
             "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": DTYPES["dense_hilo"] if info.get("field") == "hilo" and info["path"] == "dense"
-            else DTYPES[info["path"]],
+            "dtype": DTYPES[info["path"] + "_hilo"] if info.get("field") == "hilo" and
+            info["path"] + "_hilo" in DTYPES else DTYPES[info["path"]],
             "data": f"synthetic (reference generator stream, {WORKLOADS[args.workload][0]})",
             "config": {"workload": desc, "reads_per_gpu": R, "reads_total": R * world,
                        "n": n, "t_f": t_f, "path": info["path"],

@@ -45,7 +45,9 @@ extern "C" {
  * accumulator, a second lo image; about half the throughput), so the field
  * carries the full state and trajectories follow the float64 reference like
  * the fp32 sparse path (the fidelity mode).  The small path
- * (n <= 256) has fp16 operands only; the sparse path is fp32 either way. */
+ * (n <= 256) supports HILO up to n = 224 (a second operand image in shared
+ * memory; the MMA is a small part of its step); the sparse path is fp32
+ * either way. */
 #define NMFA_FIELD_FP16 0
 #define NMFA_FIELD_HILO 1
 
@@ -124,10 +126,11 @@ int nmfa_problem_create_sk_device(int64_t n, uint64_t seed, int64_t row_lo, int6
  * cannot run this problem (e.g. SMALL with n > 256). */
 int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path);
 
-/* Dense-path operand precision for plans created from now on (NMFA_FIELD_*;
- * default FP16).  Drops the problem's cached plan; existing explicit plans keep
- * the precision they were built with.  NMFA_ERR_ARG for HILO on a problem whose
- * path is SMALL, and for a row shard (its exchange carries the hi image only).
+/* Operand precision of the tensor-core paths for plans created from now on
+ * (NMFA_FIELD_*; default FP16).  Drops the problem's cached plan; existing
+ * explicit plans keep the precision they were built with.  NMFA_ERR_ARG for
+ * HILO on a small-path problem with n > 224, and for a row shard (its
+ * exchange carries the hi image only).
  * No reference counterpart: the reference computes the field in float64
  * (_kernels_numba.py:72); HILO is the closest this path gets to it. */
 int nmfa_problem_set_field_precision(nmfa_problem_t* p, int32_t field);

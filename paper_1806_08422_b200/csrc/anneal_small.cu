@@ -8,6 +8,10 @@
 // to an mbarrier; every warp then drains its TMEM lane quarter, applies the
 // fused update (reference _kernels_numba.py:71-75) and writes the new fp16
 // operand back into SMEM.  No HBM traffic inside the anneal.
+// HILO field (NMFA_FIELD_HILO): the operand is hi = fp16(s) plus a second SMEM
+// image lo = fp16(s - hi), and every K step issues one MMA per part into the
+// same accumulator, so the field sees ~22 bits of the fp32 master (np <= 224:
+// J + two operand images fit in SMEM).
 #include <cstdlib>
 #include <vector>
 
@@ -44,6 +48,7 @@ struct SmallArgs {
   float* s_out;        // [R][n] or null
   float* s_hist;       // [R][t_f][n] or null
   int cs;              // warps per TMEM lane quarter (column split)
+  int hilo;            // HILO field: second operand image (lo), two MMAs per K step
 };
 
 constexpr uint32_t kRowsPerCta = 128;
@@ -53,13 +58,32 @@ constexpr uint32_t kLboA = (kRowsPerCta / 8) * 128;  // A: K core matrices 2048 
 #define NMFA_SMALL_MINB 1  // blocks per SM the register budget targets (A/B knob)
 #endif
 
+// 16 spins of replica row rl into the operand image (fp16 hi) and, for the
+// HILO field, the residual image (fp16 lo = s - hi)
+__device__ __forceinline__ void store_operand(uint8_t* sA, uint8_t* sL, int hilo, int rl, int c0,
+                                              const float v[16]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint4 hv, lv;
+    if (hilo) {
+      split_hilo8<true>(v + 8 * h, hv, lv, false);
+      *reinterpret_cast<uint4*>(sL + kmajor_off(rl, c0 + 8 * h, kLboA)) = lv;
+    } else {
+      hv = make_uint4(pack_half2(v[8 * h + 0], v[8 * h + 1]), pack_half2(v[8 * h + 2], v[8 * h + 3]),
+                      pack_half2(v[8 * h + 4], v[8 * h + 5]), pack_half2(v[8 * h + 6], v[8 * h + 7]));
+    }
+    *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8 * h, kLboA)) = hv;
+  }
+}
+
 template <bool kInjected>
 __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(const SmallArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int np = a.np;
   uint8_t* sJ = smem;
   uint8_t* sA = smem + (size_t)np * np * 2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kRowsPerCta * np * 2);
+  uint8_t* sL = sA + (size_t)kRowsPerCta * np * 2;  // HILO: lo image (else zero bytes)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sL + (a.hilo ? (size_t)kRowsPerCta * np * 2 : 0));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -101,12 +125,7 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
       v[c] = (a.s0 && valid && i < a.n) ? a.s0[rrel * a.n + i] : 0.f;
     }
     tmem_st16(t_mst + c0, v);
-    uint4 lo = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
-                          pack_half2(v[6], v[7]));
-    uint4 hi = make_uint4(pack_half2(v[8], v[9]), pack_half2(v[10], v[11]),
-                          pack_half2(v[12], v[13]), pack_half2(v[14], v[15]));
-    *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0, kLboA)) = lo;
-    *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8, kLboA)) = hi;
+    store_operand(sA, sL, a.hilo, rl, c0, v);
   }
   tmem_wait_st();
   fence_proxy_async_smem();
@@ -114,7 +133,7 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
   __syncthreads();
 
   const uint32_t idesc = make_idesc_f16(kRowsPerCta, (uint32_t)np);
-  const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sJ);
+  const uint32_t a_addr = smem_u32(sA), l_addr = smem_u32(sL), b_addr = smem_u32(sJ);
   const uint32_t lboB = (uint32_t)np * 16u;
 
   for (int t = 0; t < a.t_f; ++t) {
@@ -124,6 +143,8 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
         uint64_t ad = make_desc_noswizzle(a_addr + ks * 2 * kLboA, kLboA, 128);
         uint64_t bd = make_desc_noswizzle(b_addr + ks * 2 * lboB, lboB, 128);
         mma_f16_ss(tbase, ad, bd, idesc, ks > 0 ? 1u : 0u);
+        if (a.hilo)
+          mma_f16_ss(tbase, make_desc_noswizzle(l_addr + ks * 2 * kLboA, kLboA, 128), bd, idesc, 1u);
       }
       mma_commit(bar);
     }
@@ -150,12 +171,7 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
         update16<kInjected>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
                             (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
       tmem_st16(t_mst + c0, ms);
-      uint4 lo = make_uint4(pack_half2(ms[0], ms[1]), pack_half2(ms[2], ms[3]),
-                            pack_half2(ms[4], ms[5]), pack_half2(ms[6], ms[7]));
-      uint4 hi = make_uint4(pack_half2(ms[8], ms[9]), pack_half2(ms[10], ms[11]),
-                            pack_half2(ms[12], ms[13]), pack_half2(ms[14], ms[15]));
-      *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0, kLboA)) = lo;
-      *reinterpret_cast<uint4*>(sA + kmajor_off(rl, c0 + 8, kLboA)) = hi;
+      store_operand(sA, sL, a.hilo, rl, c0, ms);
       if (extra && nvalid > 0) {
         if (a.s_hist) {
           float* hrow = a.s_hist + ((long long)rrel * a.t_f + t) * a.n + c0;
@@ -216,6 +232,7 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.cfg = cfg;
   a.s_out = s_out;
   a.s_hist = s_hist;
+  a.hilo = pl->field == NMFA_FIELD_HILO ? 1 : 0;
   const long long ctas = (pl->R + kRowsPerCta - 1) / kRowsPerCta;
   // Spread columns over more warps when the grid cannot fill the GPU.
   int sms = 148;
@@ -223,7 +240,7 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.cs = ctas >= sms ? 2 : 4;
   if (const char* e = getenv("NMFA_SMALL_CS")) a.cs = atoi(e);  // tuning override
   if (a.cs > p->np / 16) a.cs = p->np / 16;
-  const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 + 16;
+  const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 * (1 + a.hilo) + 16;
   auto kern = noise ? small_anneal_kernel<true> : small_anneal_kernel<false>;
   NMFA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
@@ -263,12 +280,14 @@ int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R
   a.oma = 1.0f - alpha;
   a.sigma = sigma;
   a.R = R;
+  a.hilo = 1;  // the HILO field when every instance asks for it
+  for (int k = 0; k < count; ++k) a.hilo &= ps[k]->field == NMFA_FIELD_HILO ? 1 : 0;
   const long long ctas = (R + kRowsPerCta - 1) / kRowsPerCta;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p0->device);
   a.cs = ctas * count >= sms ? 2 : 4;
   if (a.cs > p0->np / 16) a.cs = p0->np / 16;
-  const size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 + 16;
+  const size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 * (1 + a.hilo) + 16;
   NMFA_CUDA_TRY(cudaFuncSetAttribute(small_anneal_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   small_anneal_kernel<false><<<dim3((unsigned)ctas, (unsigned)count), 128 * a.cs, smem, st>>>(a);

@@ -569,9 +569,9 @@ int nmfa_problem_set_field_precision(nmfa_problem_t* p, int32_t field) {
   if (field != NMFA_FIELD_FP16 && field != NMFA_FIELD_HILO)
     return arg_error("unknown field precision " + std::to_string(field));
   std::lock_guard<std::mutex> lock(p->cache_mu);
-  if (field == NMFA_FIELD_HILO && p->path == NMFA_PATH_SMALL)
-    return arg_error("field precision HILO is built for the dense path; the small path "
-                     "(n <= 256) runs fp16 operands (set_path('dense') first)");
+  if (field == NMFA_FIELD_HILO && p->path == NMFA_PATH_SMALL && p->np > kSmallHiloMaxNp)
+    return arg_error("field precision HILO on the small path needs n <= 224 (J and two operand "
+                     "images in shared memory); set_path('dense') first");
   if (field == NMFA_FIELD_HILO && p->d_j_dense && (p->row_lo != 0 || p->row_hi != p->n))
     return arg_error("field precision HILO is not available on a row shard");
   if (p->cached_plan) {  // the cached plan was built with the old precision
@@ -596,9 +596,9 @@ int nmfa_problem_set_path(nmfa_problem_t* p, int32_t path) {
     return arg_error("a device-generated problem only runs the dense path");
   if (path == NMFA_PATH_SMALL && !p->d_j_small)
     return arg_error("small path needs n <= 256");
-  if (path == NMFA_PATH_SMALL && p->field == NMFA_FIELD_HILO)
-    return arg_error("the small path runs fp16 operands only; set the field precision to "
-                     "FP16 first");
+  if (path == NMFA_PATH_SMALL && p->field == NMFA_FIELD_HILO && p->np > kSmallHiloMaxNp)
+    return arg_error("field precision HILO on the small path needs n <= 224; set the field "
+                     "precision to FP16 first");
   if (path == NMFA_PATH_DENSE && !p->d_j_dense) {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -672,7 +672,7 @@ int nmfa_plan_create(const nmfa_problem_t* p, int64_t R, int32_t t_f, const doub
   pl->R = R;
   pl->t_f = t_f;
   pl->path = p->path;
-  pl->field = p->path == NMFA_PATH_DENSE ? p->field : NMFA_FIELD_FP16;
+  pl->field = p->path != NMFA_PATH_SPARSE ? p->field : NMFA_FIELD_FP16;
   pl->alpha = (float)alpha;
   pl->oma = (float)(1.0 - alpha);
   pl->sigma = (float)sigma;

@@ -119,6 +119,7 @@ struct nmfa_plan {
 };
 
 namespace nmfa {
+constexpr int kSmallHiloMaxNp = 224;  // small path + HILO field: J + 2 operand images in SMEM
 // kernels (launchers return NMFA_OK or an error code)
 int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noise,
                         const float* s0, int8_t* cfg, float* s_out, float* s_hist,

@@ -280,11 +280,15 @@ class _FieldPrecision:
 
 
 def _replay_field(problem, device, field):
-    """The replay mode is the fidelity mode: on the dense path it multiplies
-    the full hi + lo state (HILO field) unless the caller chose a field."""
+    """The replay mode is the fidelity mode: on the tensor-core paths it
+    multiplies the full hi + lo state (HILO field; small path up to n = 224)
+    unless the caller chose a field."""
     if field is not None:
         return field
-    return "hilo" if problem.device_handle(device).info()["path"] == "dense" else None
+    info = problem.device_handle(device).info()
+    if info["path"] == "dense" or (info["path"] == "small" and info["n"] <= 224):
+        return "hilo"
+    return None
 
 
 def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=None,
@@ -435,15 +439,15 @@ def nmfa_step(problem, s, T, params, rng):
 
     The noise comes from the caller's numpy generator, one standard normal per
     spin scaled by sigma, exactly as the reference draws it, so a shared
-    generator gives both packages the same step.  On the dense path the step
-    uses the HILO field, as the replay mode does.
+    generator gives both packages the same step.  On the tensor-core paths the
+    step uses the HILO field, as the replay mode does.
     """
     if T <= 0.0:  # the reference's test (a NaN temperature is not rejected there either)
         raise ValueError(f"temperature must be positive, got {T}")
     prob = as_problem(problem)
     drive = params.sigma * rng.standard_normal(prob.n)
     # the reference's own noise, like the replay mode: the same (HILO on the
-    # dense path) field, so t_f steps equal nmfa_run(noise="reference") bitwise
+    # tensor-core paths) field, so t_f steps equal nmfa_run(noise="reference") bitwise
     updated, _ = run_with_noise(prob, np.full(1, float(T)), drive.reshape(1, -1), params.alpha, s0=s,
                                 field=_replay_field(prob, 0, None))
     return updated
