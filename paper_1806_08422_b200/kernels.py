@@ -20,7 +20,9 @@ The device problem for a coupling matrix is built once and cached on the
 identity of the caller's arrays (a batch passes the same arrays for every
 run), so repeated calls only move s, noise and the results.  ``norm`` must be
 the problem's own normalizers (the reference always passes
-``problem.normalizers_safe``); it is checked.
+``problem.normalizers_safe``); it is checked.  The tensor-core paths run the
+HILO field here (the full state as the GEMM operand, include/nmfa_b200.h
+NMFA_FIELD_HILO): the contract is the reference's float64 kernel.
 """
 
 from __future__ import annotations
@@ -83,7 +85,7 @@ def _problem_csr(indptr, indices, weights, h):
 
 
 def _anneal(problem, norm, s, temps, noise, alpha, record):
-    from .solver import run_with_noise
+    from .solver import _replay_field, run_with_noise
 
     if not np.allclose(np.asarray(norm, dtype=np.float64), problem.normalizers_safe, rtol=1e-12,
                        atol=0.0):
@@ -91,7 +93,8 @@ def _anneal(problem, norm, s, temps, noise, alpha, record):
     s0 = np.asarray(s, dtype=np.float64)
     s_new, traj = run_with_noise(problem, np.asarray(temps, dtype=np.float64),
                                  np.asarray(noise, dtype=np.float64), float(alpha), s0=s0,
-                                 record_trajectory=bool(record))
+                                 record_trajectory=bool(record),
+                                 field=_replay_field(problem, 0, None))
     if isinstance(s, np.ndarray) and s.dtype == np.float64 and s.flags.writeable:
         s[...] = s_new  # the contract advances s in place (_kernels_numba.py:3-13)
         s_new = s

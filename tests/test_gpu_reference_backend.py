@@ -54,16 +54,18 @@ def test_reference_run_with_noise_on_b200(nmfa):
         noise = noise_stream(seed).standard_normal((t_f, p.n)) * 0.15
         s, tr = nmfa.run_with_noise(p, temps, noise, 0.15, record_trajectory=True)
         ref = T[name + "_s"]
-        assert np.max(np.abs(s - ref)) <= 2e-2, name
-        firm = np.abs(ref) > 2e-2
-        assert np.array_equal(np.sign(s[firm]), np.sign(ref[firm])), name
-        assert np.mean(tr.energies == T[name + "_e_hist"]) >= 0.9, name
+        # the backend runs the HILO field (the full state through the GEMM) and these
+        # J are exact in fp16: within 1e-5 of the reference's float64 kernel
+        assert np.max(np.abs(s - ref)) <= 1e-5, (name, np.max(np.abs(s - ref)))
+        assert np.array_equal(np.sign(s), np.sign(ref)), name
+        assert np.mean(tr.energies == T[name + "_e_hist"]) >= 0.99, name
 
 
 def test_reference_nmfa_batch_on_b200(nmfa):
     """nmfa_batch (solver.py:262-280): same per-run numpy noise streams as the
-    reference's numba run, so almost every run ends in the same energy; every
-    returned energy is the reference's own energy() of the returned config."""
+    reference's numba run, so (HILO field) all but at most one run in 32 end
+    in the same energy; every returned energy is the reference's own energy()
+    of the returned config."""
     B = load("batches.npz")
     for name, p, t_f, R in [("moebius16_tf100", nmfa.moebius_ladder(16), 100, 100),
                             ("cubic40_tf300", nmfa.gen_cubic_maxcut(40, 1), 300, 32),
@@ -72,7 +74,7 @@ def test_reference_nmfa_batch_on_b200(nmfa):
         e = np.array([r.final_energy for r in res])
         assert [r.seed for r in res] == list(range(R))
         assert all(r.final_energy == nmfa.energy(p, r.final_config) for r in res)
-        assert np.mean(e == B[name + "_E"]) >= 0.9, (name, np.mean(e == B[name + "_E"]))
+        assert np.mean(e == B[name + "_E"]) >= 0.95, (name, np.mean(e == B[name + "_E"]))
 
 
 def test_reference_brute_force_ground_on_b200(nmfa):
