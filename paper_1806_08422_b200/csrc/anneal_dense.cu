@@ -1065,43 +1065,56 @@ int dense_plan_alloc(nmfa_plan* pl) {
   ds->slice_lo = (int)(p->row_lo / kBK);
   ds->slice_hi = (int)((p->row_hi + kBK - 1) / kBK);
   const long long upm = p->brows / 16, mb = ds->Rp / 256;
+  // Tile width for a group of `blocks` replica blocks: minimise the makespan
+  // ceil(tiles / pairs) * cost(w) of the cost model above.
+  auto width_for = [&](long long blocks) {
+    int bw = kMaxW;
+    double bc = 1e300;
+    for (int w = 1; w <= kMaxW; ++w) {
+      const long long tpm = (upm + w - 1) / w, T = tpm * blocks;
+      const long long pairs_used = std::min<long long>(sms / 2, T);
+      const double per_slice = std::max(64.0 * w, 563.0 + 22.6 * w);
+      const double makespan = (double)((T + pairs_used - 1) / pairs_used) * per_slice;
+      if (makespan < bc - 1e-9) {
+        bc = makespan;
+        bw = w;
+      }
+    }
+    return bw;
+  };
   // L2-aware replica groups: replica blocks never interact, so when the
   // working set of one sweep (two hi images + lo + J) outgrows L2 the blocks
   // are split into groups annealed one after another (one persistent launch
-  // each, all t_f sweeps), as long as each group still deals >= 2 tiles to
-  // every pair.  Results are unchanged (natural K order, global replica keys).
-  // profiles/r02/dense_groups.log: N x R beyond L2 fell to 0.65-0.70 of the
-  // sustained peak as one group.  Row-sharded plans advance sweep by sweep
-  // across devices and stay one group.  NMFA_DENSE_GROUPS=k forces k groups,
-  // NMFA_L2_BUDGET_MB sets the budget.
+  // each, all t_f sweeps), as long as every group still deals >= 3.75 tiles
+  // per pair: below that a sweep is bound by its dependency chain (a tile's
+  // MMA, then its epilogue, then the next sweep's wait), not by L2, and the
+  // split lost up to 14% at N = 1000-1500 (profiles/r02/dense_groups.log).
+  // Results are unchanged (natural K order, global replica keys).  N x R
+  // beyond L2 fell to 0.65-0.70 of the sustained peak as one group.
+  // Row-sharded plans advance sweep by sweep across devices and stay one
+  // group.  NMFA_DENSE_GROUPS=k forces k groups, NMFA_L2_BUDGET_MB sets the
+  // budget.
   const double j_bytes = (double)ds->kp * p->brows * 2.0;
   const double images = ds->hilo ? 4.0 : 3.0;  // two hi images + lo (+ the second lo of HILO)
   auto footprint = [&](long long blocks) { return images * 2.0 * ds->kp * 256.0 * blocks + j_bytes; };
   static const char* budget_env = getenv("NMFA_L2_BUDGET_MB");
   const double budget = (budget_env ? atof(budget_env) : 120.0) * 1e6;
-  const long long tpm_est = (upm + 13) / 14;
+  auto tiles_for = [&](long long blocks) {
+    const int w = width_for(blocks);
+    return (upm + w - 1) / w * blocks;
+  };
   long long n_groups = 1;
   if (!dense_is_sharded(p)) {
     while (footprint((mb + n_groups - 1) / n_groups) > budget) {
       const long long g2 = n_groups * 2;
-      if (g2 > mb || (mb / g2) * tpm_est < 2LL * (sms / 2)) break;
+      if (g2 > mb || 4 * tiles_for(mb / g2) < 15LL * (sms / 2)) break;  // >= 3.75 per pair
       n_groups = g2;
     }
   }
   static const char* groups_env = getenv("NMFA_DENSE_GROUPS");
   if (groups_env && atoi(groups_env) >= 1) n_groups = std::min<long long>(mb, atoi(groups_env));
   const long long mb_g = (mb + n_groups - 1) / n_groups;  // largest group
-  int best_w = kMaxW;  double best_cost = 1e300;
-  for (int w = 1; w <= kMaxW; ++w) {
-    const long long tpm = (upm + w - 1) / w, T = tpm * mb_g;
-    const long long pairs_used = std::min<long long>(sms / 2, T);
-    const double per_slice = std::max(64.0 * w, 563.0 + 22.6 * w);
-    const double makespan = (double)((T + pairs_used - 1) / pairs_used) * per_slice;
-    if (makespan < best_cost - 1e-9) {
-      best_cost = makespan;
-      best_w = w;
-    }
-  }
+  int best_w = width_for(mb_g);
   static const char* w_env = getenv("NMFA_TILE_W");  // experiment: force the tile width
   if (w_env && atoi(w_env) >= 1 && atoi(w_env) <= kMaxW) best_w = atoi(w_env);
   const long long tpm = (upm + best_w - 1) / best_w;
