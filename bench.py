@@ -10,11 +10,14 @@ the end).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload k2000|sk100|moebius100|g2000|moebius131072|torus|ground26|sk65536]
+                    [--reads R] [--field fp16|hilo]
 
-Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle port
-of the reference's per-run loop (oracle/nmfa_oracle.py, which follows
-solver.py:236-280 / _kernels_numba.py:64-80) on this host's cores, on a
-bounded sample of the same workload.
+Prints ONE JSON line on rank 0.  --impl reference times the reference's own
+per-run loop (`nmfa.nmfa_batch` from the unmodified install in baseline/_ref,
+solver.py:236-280 / _kernels_numba.py:64-80; when that install is missing,
+the oracle's jitted restatement, oracle/nmfa_oracle.py) on this host's cores,
+on a bounded sample of the same workload.  --field hilo measures the dense
+path's fidelity mode (NMFA_FIELD_HILO) instead of the default fp16 operand.
 """
 
 import argparse
