@@ -77,7 +77,11 @@ __global__ void __launch_bounds__(64, 1)
         for (uint32_t r = 0; r < CS; ++r) {
           uint32_t a;
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(&empty[s])), "r"(r));
+#ifdef RELAXED_ARRIVE  // the consumer frees the slot with relaxed remote arrives (no cluster release)
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+#else
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+#endif
         }
       }
     }
@@ -120,7 +124,12 @@ void run(void* buf, long long lines, int tile_lines, unsigned long long* clk) {
   double mean = 0;
   for (int i = 0; i < grid; ++i) mean += (double)h[i] / grid;
   const double per = mean / iters;
-  printf("stages %d cluster %d %-9s tile %3d KB (box %2d KB)  err=%d  %7.1f clk/stage  %6.1f B/clk/SM delivered, %6.1f B/clk/SM issued\n",
+  printf("%s stages %d cluster %d %-9s tile %3d KB (box %2d KB)  err=%d  %7.1f clk/stage  %6.1f B/clk/SM delivered, %6.1f B/clk/SM issued\n",
+#ifdef RELAXED_ARRIVE
+         "relaxed",
+#else
+         "release",
+#endif
          kStages, CS, MC ? "multicast" : "unicast", tile_lines / 8, box / 8, (int)err, per, tile_lines * 128 / per,
          box * 128 / per);
 }
