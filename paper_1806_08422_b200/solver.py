@@ -297,8 +297,10 @@ def sample(problem, params=None, n_runs=1, *, r0=0, device=0, noise=None, s0=Non
 
     noise: optional (n_runs, t_f, n) pre-scaled additive noise (device tensor
     or array); when given, params.sigma is unused (run_with_noise seam).
-    field: dense-path GEMM operand for this call, "fp16" or "hilo" (None: the
-    problem's setting, default "fp16"; include/nmfa_b200.h NMFA_FIELD_*).
+    field: tensor-core GEMM operand for this call, "fp16" or "hilo" (None: the
+    problem's setting, default "fp16"; include/nmfa_b200.h NMFA_FIELD_*).  It
+    switches the problem's setting for the duration of the call, so threads
+    sharing one problem should not pass different fields concurrently.
     """
     problem = as_problem(problem)
     with _FieldPrecision(problem, device, field):
