@@ -43,10 +43,12 @@ def margins_ok(raw):
     return bool(np.all(r[:MARGIN] == 0x5A) and np.all(r[-MARGIN:] == 0x5A))
 
 
-def c_anneal(name, prob, R, t_f, seed, r0=0, path=None, hist=False, noise=None):
+def c_anneal(name, prob, R, t_f, seed, r0=0, path=None, hist=False, noise=None, field=None):
     """Direct nmfa_anneal with redzoned caller buffers."""
     if path:
         prob.device_handle().set_path(path)
+    if field:
+        prob.device_handle().set_field_precision(field)
     n = prob.n
     temps = np.ascontiguousarray(nb.DEFAULT_SCHEDULE.temperatures(t_f))
     bufs = {"cfg": guarded((R, n), torch.int8), "e": guarded((R,), torch.float64),
@@ -78,6 +80,11 @@ c_anneal("dense_hist", nb.gen_sk(300, 2), 64, T, 5, path="dense", hist=True)
 rng = np.random.default_rng(4)
 c_anneal("dense_inj", nb.gen_sk(520, 5), 33, T, 0, path="dense",
          noise=rng.standard_normal((33, T, 520)) * 0.15)
+# HILO field: the second lo image (ping-pong) and two MMAs per k-slice / K step
+c_anneal("dense_hilo", nb.gen_sk(600, 1), 300, T, 5, path="dense", field="hilo", hist=True)
+c_anneal("dense_hilo_inj", nb.gen_sk(520, 5), 33, T, 0, path="dense", field="hilo",
+         noise=rng.standard_normal((33, T, 520)) * 0.15)
+c_anneal("small_hilo", nb.gen_sk(100, 0), 300, T, 3, field="hilo", hist=True)
 c_anneal("ell", nb.moebius_ladder(1000), 100, T, 7)                             # degree-3 ELL kernel
 c_anneal("ell_hist", nb.moebius_ladder(600), 37, T, 7, hist=True)
 c_anneal("csr", nb.gen_dense_maxcut(1200, 0.01, 2), 70, T, 9, path="sparse")   # CSR kernel
