@@ -27,6 +27,8 @@ def test_null_handles_are_rejected():
     assert lib.nmfa_ground_state(None, 26, None, None, None) == ARG
     assert lib.nmfa_anneal_many(None, 0, 4, 10, None, 0.15, 0.15, None, None, None, None) == ARG
     assert lib.nmfa_best_of(None, 0, None, None, None) != 0
+    assert lib.nmfa_problem_set_field_precision(None, 1) == ARG
+    assert "NULL" in err()
 
 
 def test_problem_validation_messages():
