@@ -692,6 +692,10 @@ def run_ours(args):
             # tensor duty per clock: FLOP/clk/SM over the 8192 dense f16 FLOP/clk/SM
             roof["per_clock_duty"] = achieved * 1e12 / (148 * sm_mhz * 1e6) / 8192
             roof["per_clock_sm_mhz"] = sm_mhz
+        if args.field == "hilo":
+            roof["note_hilo"] = ("HILO field: the kernel issues two MMAs per k-slice (hi and lo), so the "
+                                 "tensor work executed is 2x the algorithmic FLOP counted here "
+                                 f"(executed-FLOP fraction {2 * achieved / peak:.3f})")
         if info["path"] == "small":
             roof["note"] = ("n <= 256 runs on chip for all t_f steps; the binding resource is the fused "
                             "update's instruction issue (ncu: 28 instructions per spin-update, IPC 2.1 "
