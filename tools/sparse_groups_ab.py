@@ -1,6 +1,8 @@
 """ELL step time with the replica slices annealed in groups (NMFA_SPARSE_GROUPS,
 direct launches) against one launch per step over all slices (also direct):
-Moebius n = 131,072 and the 362x362 torus, 1024 reads, t_f = 200."""
+Moebius n = 131,072 and the 362x362 torus, 1024 reads, t_f = 200.  The
+NMFA_SPARSE_GROUPS patch of anneal_sparse.cu was reverted after this study
+(profiles/r02/sparse_replica_groups.log); without it the variable is ignored."""
 import os
 import sys
 
