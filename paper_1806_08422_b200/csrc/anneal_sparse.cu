@@ -22,6 +22,9 @@
 #ifndef NMFA_CSR_ROUNDS
 #define NMFA_CSR_ROUNDS 2
 #endif
+#ifndef NMFA_CSR_ROUNDS_LONG
+#define NMFA_CSR_ROUNDS_LONG 2  // A/B knob: 3 gave +10% at degree 10 but -7% on the staged path
+#endif
 #ifndef NMFA_FULL_GROUP_STORES
 #define NMFA_FULL_GROUP_STORES 1  // unpredicated state stores for interior groups (+1%)
 #endif
@@ -220,6 +223,9 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   // first use (degree <= kFast unrolled, longer rows in a general loop).
   constexpr int kFast = 3;  // unrolled row length (cubic / Moebius ladder); longer rows loop
   constexpr int kRounds = NMFA_CSR_ROUNDS;  // entries per row gathered per round beyond kFast
+  // segments beyond the staged size (mean degree > 8); 3 entries per row per round trip
+  // measured +10% at degree 10 but cost the staged path 7% (register allocation), so 2
+  constexpr int kRoundsLong = V == 2 ? NMFA_CSR_ROUNDS_LONG : NMFA_CSR_ROUNDS;  // V = 1 would spill
   const int i_base = 8 * q;
   const int pl = lane <= 8 ? __ldg(a.ptr + min(i_base + lane, n)) : 0;
   int k0[8], deg[8];
@@ -379,10 +385,10 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     int dmax = 0;
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) dmax = max(dmax, deg[qq]);
-    for (int u = kFast; u < dmax; u += kRounds) {
-      float x[kRounds][8][V], wv[kRounds][8];
+    for (int u = kFast; u < dmax; u += kRoundsLong) {
+      float x[kRoundsLong][8][V], wv[kRoundsLong][8];
 #pragma unroll
-      for (int j = 0; j < kRounds; ++j)
+      for (int j = 0; j < kRoundsLong; ++j)
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq) {
           if (u + j < deg[qq]) {
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
           }
         }
 #pragma unroll
-      for (int j = 0; j < kRounds; ++j)
+      for (int j = 0; j < kRoundsLong; ++j)
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
           if (u + j < deg[qq])
