@@ -9,7 +9,7 @@ sharded with no data-path collective; one all-gather of each rank's best at
 the end).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload k2000|sk100|moebius100|g2000|moebius131072|torus|ground26|sk65536]
+                    [--workload k2000|sk100|moebius100|g2000|moebius131072|torus|gset5000|ground26|sk65536]
                     [--reads R] [--field fp16|hilo]
 
 Prints ONE JSON line on rank 0.  --impl reference times the reference's own
@@ -47,6 +47,11 @@ WORKLOADS = {
     # the G-set toroidal class at scale (degree 4: ELL kernel with 4 slots)
     "torus": ("toroidal_grid(362, 362, 1)", 131044, 1024, 200,
               "toroidal grid 362x362 (n=131044, +-1 couplers, sparse ELL path), 1024 reads/GPU, t_f=200"),
+    # the G-set random class beyond the dense crossover (G55/G60 shape: n = 5000, mean degree 5,
+    # max degree > 4): the CSR kernel with staged segments
+    "gset5000": ("gen_dense_maxcut(5000, 5.0 / 4999, 1)", 5000, 4096, 1000,
+                 "G-set-class random graph gen_dense_maxcut(5000, 0.001, 1) (mean degree 5, sparse CSR "
+                 "path), 4096 reads/GPU, t_f=1000"),
     # exhaustive ground state (brute_force_ground) at the reference's limit
     "ground26": ("gen_sk(26, 1)", 26, 1, 1, "exact ground state of gen_sk(26,1) by Gray-code enumeration"),
     # config 5: J generated on device, row-sharded over the ranks (strong scaling)
@@ -206,7 +211,7 @@ def cpu_reference(workload, sample_runs=None, threads=None):
     p = build_problem(inst, workload)
     threads = threads or os.cpu_count() or 1
     if sample_runs is None:
-        sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads,
+        sample_runs = {"k2000": 2 * threads, "g2000": 8 * threads, "gset5000": 8 * threads,
                        "moebius131072": threads, "torus": threads}.get(workload, 64 * threads)
     nmfa = reference_package()
     if nmfa is not None:
