@@ -78,6 +78,12 @@ namespace nmfa {
 #ifndef NMFA_DSTAGES
 #define NMFA_DSTAGES 3
 #endif
+#ifndef NMFA_PF_SLEEP_NS
+#define NMFA_PF_SLEEP_NS 20  // producer's back-off while its next slice is not yet known ready
+#endif
+#ifndef NMFA_POLL_SLEEP_NS
+#define NMFA_POLL_SLEEP_NS 32  // prefetch thread's back-off between readiness polls
+#endif
 constexpr int kDStages = NMFA_DSTAGES;
 constexpr int kBK = 128;  // K per pipeline stage: one 32 KB TMA box per operand
 #ifndef NMFA_EPI_WARPS
@@ -417,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               // one shared-memory load instead of a round of L2 polls and fences
               do {
                 seen = ld_acquire_cta_smem(&pf_ready);
-                if (seen < step + (unsigned long long)(ki + 1)) __nanosleep(20);
+                if (seen < step + (unsigned long long)(ki + 1)) __nanosleep(NMFA_PF_SLEEP_NS);
               } while (seen < step + (unsigned long long)(ki + 1));
               fence_proxy_async_global();
             }
@@ -558,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
               fence_acq_rel_gpu();  // acquire the published slices for this CTA
               st_release_cta_smem(&pf_ready, (step << 16) | (unsigned long long)known);
             } else {
-              __nanosleep(32);
+              __nanosleep(NMFA_POLL_SLEEP_NS);
             }
           }
           done_m = tl.m_blk;
