@@ -110,7 +110,14 @@ constexpr int kMaxW = NMFA_DMAXW;
 constexpr uint32_t kBTileMax = 8 * kMaxW * kBK * 2;  // <= 8 * kMaxW rows (N/2) x 128 k
 constexpr uint32_t kDStageBytes = kATile + kBTileMax;
 constexpr uint32_t kAccCols = 256;
-constexpr size_t kDSmemBytes = (size_t)kDStages * kDStageBytes + 1024;
+// Box-Muller (sin, cos) table of the 4096 noise angles after the ring (common.cuh
+// sincos_table_fill: bitwise the inline MUFU values), when it fits
+constexpr size_t kDRingBytes = (size_t)kDStages * kDStageBytes;
+#ifndef NMFA_DENSE_TABLE
+#define NMFA_DENSE_TABLE 0  // measured neutral at K2000, -8% at small N (the 32 KB it takes from L1)
+#endif
+constexpr bool kDTab = NMFA_DENSE_TABLE && kDRingBytes + 4096 * 8 + 2048 <= 227 * 1024;
+constexpr size_t kDSmemBytes = kDRingBytes + 1024;  // the table is static shared memory
 
 struct DenseTile {
   int m_blk, n0, nlen, pad;
@@ -383,6 +390,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
     fence_mbar_init();
     pf_ready = 0;
   }
+  // static, so its address is an immediate (no register in the 96-register epilogue)
+  __shared__ float2 sTab[kDTab ? 4096 : 1];
+  if (kDTab) sincos_table_fill(sTab, threadIdx.x, blockDim.x);
   if (warp == kWarpAlloc) tmem_alloc_pair(&tmem_slot, 2 * kAccCols);
   tc_fence_before();
   cluster_sync_all();
@@ -718,8 +728,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
 #pragma unroll
             for (int cc = 0; cc < W; ++cc) ms[cc] = fmaf(acc[cc], 1e-6f, ms[cc]);
 #else
-            update_chunk<kInjected, W>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
-                                       (uint32_t)(i0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+            update_chunk<kInjected, W, kDTab>(acc, ms, invn4 + i0 / 4, hn4 + i0 / 4, nz, nvalid, K,
+                                              (uint32_t)(i0 / 8), (uint32_t)t, a.sigma, inv_t,
+                                              a.alpha, a.oma, sTab);
 #endif
             // split s -> (hi, lo); the last sweep writes the +-1 configuration for the energy pass
 #pragma unroll

@@ -12,6 +12,7 @@
 // image lo = fp16(s - hi), and every K step issues one MMA per part into the
 // same accumulator, so the field sees ~22 bits of the fp32 master (np <= 224:
 // J + two operand images fit in SMEM).
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -76,14 +77,18 @@ __device__ __forceinline__ void store_operand(uint8_t* sA, uint8_t* sL, int hilo
   }
 }
 
-template <bool kInjected>
+// kTab: the Box-Muller (sin, cos) of the 4096 noise angles come from a 32 KB
+// shared-memory table built at launch with the same MUFU instructions (bitwise
+// the same normals, two XU operations fewer per pair); used when it fits.
+template <bool kInjected, bool kTab>
 __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(const SmallArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int np = a.np;
   uint8_t* sJ = smem;
   uint8_t* sA = smem + (size_t)np * np * 2;
   uint8_t* sL = sA + (size_t)kRowsPerCta * np * 2;  // HILO: lo image (else zero bytes)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sL + (a.hilo ? (size_t)kRowsPerCta * np * 2 : 0));
+  float2* sTab = reinterpret_cast<float2*>(sL + (a.hilo ? (size_t)kRowsPerCta * np * 2 : 0));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTab) + (kTab ? 4096 * 8 : 0));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -100,6 +105,7 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
 
   for (uint32_t i = tid; i < a.j_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(sJ)[i] = j_img[i];
+  if (kTab) sincos_table_fill(sTab, tid, blockDim.x);  // visible after the __syncthreads below
   if (warp == 0) tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -165,11 +171,13 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
       const int nvalid = valid ? min(16, a.n - c0) : 0;
       const float* nz = kInjected ? a.noise + ((long long)rrel * a.t_f + t) * a.n + c0 : nullptr;
       if (a.n - c0 <= 8)  // the padded tail chunk: columns >= n only meet zero J columns
-        update_chunk<kInjected, 8>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
-                                   (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+        update_chunk<kInjected, 8, kTab>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
+                                         (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha,
+                                         a.oma, sTab);
       else
-        update16<kInjected>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
-                            (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma);
+        update16<kInjected, kTab>(acc, ms, invn4 + c0 / 4, hn4 + c0 / 4, nz, nvalid, K,
+                                  (uint32_t)(c0 / 8), (uint32_t)t, a.sigma, inv_t, a.alpha, a.oma,
+                                  sTab);
       tmem_st16(t_mst + c0, ms);
       store_operand(sA, sL, a.hilo, rl, c0, ms);
       if (extra && nvalid > 0) {
@@ -200,6 +208,18 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
     tc_fence_after();
     tmem_dealloc(tbase, a.tmem_cols);
   }
+}
+
+constexpr size_t kTabBytes = 4096 * sizeof(float2);
+// the sincos table is used when it fits beside J and the operand image(s), at
+// two CTAs per SM while the image alone allowed two (NMFA_SMALL_TABLE=0: never)
+static bool small_table_fits(size_t smem) {
+  static const char* env = getenv("NMFA_SMALL_TABLE");
+  if (env && env[0] == '0') return false;
+  const size_t per_sm = 228 * 1024, per_cta = 227 * 1024;
+  const int ctas_before = (int)std::min<size_t>(2, per_sm / (smem + 1024));
+  const int ctas_after = (int)std::min<size_t>(2, per_sm / (smem + kTabBytes + 1024));
+  return smem + kTabBytes <= per_cta && ctas_after >= ctas_before;
 }
 
 static uint32_t pow2_cols(uint32_t c) {
@@ -240,8 +260,11 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   a.cs = ctas >= sms ? 2 : 4;
   if (const char* e = getenv("NMFA_SMALL_CS")) a.cs = atoi(e);  // tuning override
   if (a.cs > p->np / 16) a.cs = p->np / 16;
-  const size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 * (1 + a.hilo) + 16;
-  auto kern = noise ? small_anneal_kernel<true> : small_anneal_kernel<false>;
+  size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 * (1 + a.hilo) + 16;
+  const bool tab = !noise && small_table_fits(smem);
+  if (tab) smem += kTabBytes;
+  auto kern = noise ? small_anneal_kernel<true, false>
+                    : (tab ? small_anneal_kernel<false, true> : small_anneal_kernel<false, false>);
   NMFA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)ctas, 128 * a.cs, smem, st>>>(a);
   NMFA_LAUNCH_CHECK();
@@ -287,10 +310,12 @@ int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p0->device);
   a.cs = ctas * count >= sms ? 2 : 4;
   if (a.cs > p0->np / 16) a.cs = p0->np / 16;
-  const size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 * (1 + a.hilo) + 16;
-  NMFA_CUDA_TRY(cudaFuncSetAttribute(small_anneal_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  small_anneal_kernel<false><<<dim3((unsigned)ctas, (unsigned)count), 128 * a.cs, smem, st>>>(a);
+  size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 * (1 + a.hilo) + 16;
+  const bool tab = small_table_fits(smem);
+  if (tab) smem += kTabBytes;
+  auto kern = tab ? small_anneal_kernel<false, true> : small_anneal_kernel<false, false>;
+  NMFA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3((unsigned)ctas, (unsigned)count), 128 * a.cs, smem, st>>>(a);
   NMFA_LAUNCH_CHECK();
   add_launches(1);
   NMFA_CUDA_TRY(cudaFreeAsync(d_inst, st));

@@ -121,11 +121,32 @@ constexpr uint32_t kNoiseTag = 0x4E4D4641u;
 // u2 = k 2^-12 (equispaced angles: E[cos^2] = 1/2, E[cos^4] = 3/8 exactly).
 // sigma is folded into the radius: r = sqrt(lgs * lg2(u1)) with
 // lgs = -2 ln 2 sigma^2 = sigma * sqrt(-2 ln u1); sigma = 0 gives z = +-0.
-__device__ __forceinline__ void box_muller(uint32_t w, float lgs, float& z0, float& z1) {
+// kTab: (sin, cos) of the 4096 angles read from a shared-memory table that
+// sincos_table_fill built with the SAME instructions, so the normals are bitwise
+// those of the inline MUFU.SIN/COS path (two XU operations fewer per pair).
+__device__ __forceinline__ void sincos_angle(uint32_t k, float& sn, float& cs) {
+  NMFA_SINCOS((float)k * 1.5339807878856412e-03f, sn, cs);  // 2 pi k / 4096
+}
+__device__ __forceinline__ void sincos_table_fill(float2* tab, int tid, int nthreads) {
+  for (int k = tid; k < 4096; k += nthreads) {
+    float sn, cs;
+    sincos_angle((uint32_t)k, sn, cs);
+    tab[k] = make_float2(sn, cs);
+  }
+}
+template <bool kTab = false>
+__device__ __forceinline__ void box_muller(uint32_t w, float lgs, float& z0, float& z1,
+                                           const float2* tab = nullptr) {
   const float u1 = fmaf((float)(w >> 12), 9.5367431640625e-07f, 4.76837158203125e-07f);
   const float r = sqrt_approx(lgs * lg2_approx(u1));
   float sn, cs;
-  NMFA_SINCOS((float)(w & 0xFFFu) * 1.5339807878856412e-03f, sn, cs);  // 2 pi k / 4096
+  if constexpr (kTab) {
+    const float2 t = tab[w & 0xFFFu];
+    sn = t.x;
+    cs = t.y;
+  } else {
+    sincos_angle(w & 0xFFFu, sn, cs);
+  }
   z0 = r * cs;
   z1 = r * sn;
 }
@@ -133,24 +154,26 @@ __device__ __forceinline__ float bm_scale(float sigma) { return -1.3862943611198
 
 // Eight N(0, sigma^2) normals for spins 8q..8q+7 of replica key K at step t:
 // one Philox4x32-10 call, one Box-Muller pair per output word.
+template <bool kTab = false>
 __device__ __forceinline__ void normal8(const PhiloxKey& K, uint32_t q, uint32_t t, float lgs,
-                                        float z[8]) {
+                                        float z[8], const float2* tab = nullptr) {
   const uint4_ w = philox4x32_10(q, t, kNoiseTag, 0u, K);
-  box_muller(w.x, lgs, z[0], z[1]);
-  box_muller(w.y, lgs, z[2], z[3]);
-  box_muller(w.z, lgs, z[4], z[5]);
-  box_muller(w.w, lgs, z[6], z[7]);
+  box_muller<kTab>(w.x, lgs, z[0], z[1], tab);
+  box_muller<kTab>(w.y, lgs, z[2], z[3], tab);
+  box_muller<kTab>(w.z, lgs, z[4], z[5], tab);
+  box_muller<kTab>(w.w, lgs, z[6], z[7], tab);
 }
 
 // The fused update of W (8 or 16) consecutive spins i0..i0+W-1 of one replica.
 //   invn4 / hn4 point at the padded per-spin constants for i0 (4-aligned).
 //   kInjected: z comes from `nz` (pre-scaled, may be unaligned, indices < n_valid)
 //   else in-kernel Philox noise scaled by sigma (q0 = i0 / 8; i0 8-aligned).
-template <bool kInjected, int W>
+template <bool kInjected, int W, bool kTab = false>
 __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const float4* invn4,
                                              const float4* hn4, const float* nz, int n_valid,
                                              const PhiloxKey& K, uint32_t q0, uint32_t t,
-                                             float sigma, float inv_t, float alpha, float oma) {
+                                             float sigma, float inv_t, float alpha, float oma,
+                                             const float2* tab = nullptr) {
   float z[W];
   if (kInjected) {
 #pragma unroll
@@ -158,7 +181,7 @@ __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const 
   } else {
     const float lgs = bm_scale(sigma);
 #pragma unroll
-    for (int q = 0; q < W / 8; ++q) normal8(K, q0 + q, t, lgs, &z[8 * q]);
+    for (int q = 0; q < W / 8; ++q) normal8<kTab>(K, q0 + q, t, lgs, &z[8 * q], tab);
   }
 #pragma unroll
   for (int q = 0; q < W / 4; ++q) {
@@ -170,12 +193,14 @@ __device__ __forceinline__ void update_chunk(const float* acc, float* ms, const 
   }
 }
 
-template <bool kInjected>
+template <bool kInjected, bool kTab = false>
 __device__ __forceinline__ void update16(const float acc[16], float ms[16], const float4* invn4,
                                          const float4* hn4, const float* nz, int n_valid,
                                          const PhiloxKey& K, uint32_t q0, uint32_t t,
-                                         float sigma, float inv_t, float alpha, float oma) {
-  update_chunk<kInjected, 16>(acc, ms, invn4, hn4, nz, n_valid, K, q0, t, sigma, inv_t, alpha, oma);
+                                         float sigma, float inv_t, float alpha, float oma,
+                                         const float2* tab = nullptr) {
+  update_chunk<kInjected, 16, kTab>(acc, ms, invn4, hn4, nz, n_valid, K, q0, t, sigma, inv_t, alpha,
+                                    oma, tab);
 }
 
 // ---------------------------------------------------------------------------
