@@ -42,6 +42,10 @@ constexpr bool kDisableStaged = true;
 #else
 constexpr bool kDisableStaged = false;
 #endif
+#ifndef NMFA_CSR_STAGED96
+#define NMFA_CSR_STAGED96 0  // A/B: a separate staged branch for 65-96 entries (3 registers)
+#endif
+constexpr bool kStaged96 = NMFA_CSR_STAGED96;
 #ifndef NMFA_SPARSE_MINB
 #define NMFA_SPARSE_MINB 4  // blocks per SM the register budget targets
 #endif
@@ -301,6 +305,79 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     const float wB = lane + 32 < seg ? __ldg(wts + K0 + 32 + lane) : 0.f;
     auto off_of = [&](int e) { return __shfl_sync(0xffffffffu, e < 32 ? offA : offB, e & 31); };
     auto w_of = [&](int e) { return __shfl_sync(0xffffffffu, e < 32 ? wA : wB, e & 31); };
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+      for (int u = 0; u < kFast; ++u) {
+        const int off = off_of(k0[qq] - K0 + u);  // unconditional: no branch around the shuffle
+        if (u < deg[qq]) {
+          ld(off, v[qq][u]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
+        }
+      }
+    sparse_noise<V>(a, q, r, z);  // overlaps the gathers' latency
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      float s2[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) s2[c] = 0.f;
+#pragma unroll
+      for (int u = 0; u < kFast; ++u) {
+        const float wv = w_of(k0[qq] - K0 + u);
+        if (u < deg[qq])
+#pragma unroll
+          for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);  // CSR order
+      }
+#pragma unroll
+      for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
+    }
+    int dmax = 0;
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) dmax = max(dmax, deg[qq]);
+    for (int u = kFast; u < dmax; u += kRounds) {
+      float x[kRounds][8][V], wv[kRounds][8];
+#pragma unroll
+      for (int j = 0; j < kRounds; ++j)
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          if (u + j < deg[qq]) {  // warp-uniform
+            const int e = k0[qq] - K0 + u + j;
+            ld(off_of(e), x[j][qq]);
+            wv[j][qq] = w_of(e);
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < kRounds; ++j)
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          if (u + j < deg[qq])
+#pragma unroll
+            for (int c = 0; c < V; ++c) acc[qq][c] = fmaf(wv[j][qq], x[j][qq][c], acc[qq][c]);
+    }  } else if (kStaged96 && seg <= 96 && !kDisableStaged) {
+    // Staged segment (rows longer than kFast, up to 64 entries per group:
+    // G-set-class random graphs of mean degree 2-8): every lane holds two
+    // entries of the segment, offsets pre-multiplied, loaded with ONE coalesced
+    // round trip; each gather then takes its offset and weight by shuffle
+    // instead of a dependent global index load (one L2 round trip per round
+    // instead of two).  Same entries, same per-row CSR order from +0: bitwise
+    // the unstaged path.  Measured (tools/csr_probe.py): +20-25% at mean degree
+    // 5, +12% at degree 2.  Not better: staging in shared memory with broadcast
+    // loads (= unstaged), 3-4 registers per lane for 96-128 entries (local
+    // memory; slower than unstaged).
+    const int offA = lane < seg ? __ldg(idx + K0 + lane) * Rp : 0;
+    const int offB = lane + 32 < seg ? __ldg(idx + K0 + 32 + lane) * Rp : 0;
+    const float wA = lane < seg ? __ldg(wts + K0 + lane) : 0.f;
+    const float wB = lane + 32 < seg ? __ldg(wts + K0 + 32 + lane) : 0.f;
+    const int offC = lane + 64 < seg ? __ldg(idx + K0 + 64 + lane) * Rp : 0;
+    const float wC = lane + 64 < seg ? __ldg(wts + K0 + 64 + lane) : 0.f;
+    auto off_of = [&](int e) {
+      return __shfl_sync(0xffffffffu, e < 32 ? offA : (e < 64 ? offB : offC), e & 31);
+    };
+    auto w_of = [&](int e) {
+      return __shfl_sync(0xffffffffu, e < 32 ? wA : (e < 64 ? wB : wC), e & 31);
+    };
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
