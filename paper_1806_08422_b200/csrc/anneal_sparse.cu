@@ -42,10 +42,7 @@ constexpr bool kDisableStaged = true;
 #else
 constexpr bool kDisableStaged = false;
 #endif
-#ifndef NMFA_CSR_STAGED96
-#define NMFA_CSR_STAGED96 0  // A/B: a separate staged branch for 65-96 entries (3 registers)
-#endif
-constexpr bool kStaged96 = NMFA_CSR_STAGED96;
+
 #ifndef NMFA_SPARSE_MINB
 #define NMFA_SPARSE_MINB 4  // blocks per SM the register budget targets
 #endif
@@ -196,7 +193,7 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
 // halving the per-update address arithmetic and the uniform CSR overhead of
 // the V = 1 layout (the CSR path is issue-bound; profiles/r01/korder_ab.log).
 // Per replica the arithmetic and summation order are the same for any V.
-template <int V>
+template <int V, bool k96 = false>
 __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     sparse_step_kernel(const SparseStepArgs a) {
   using Vec = typename std::conditional<V == 2, float2, float>::type;
@@ -288,7 +285,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
     }
-  } else if (seg <= 64 && !kDisableStaged) {
+  } else if (seg <= (k96 ? 96 : 64) && !kDisableStaged) {
     // Staged segment (rows longer than kFast, up to 64 entries per group:
     // G-set-class random graphs of mean degree 2-8): every lane holds two
     // entries of the segment, offsets pre-multiplied, loaded with ONE coalesced
@@ -303,80 +300,15 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     const int offB = lane + 32 < seg ? __ldg(idx + K0 + 32 + lane) * Rp : 0;
     const float wA = lane < seg ? __ldg(wts + K0 + lane) : 0.f;
     const float wB = lane + 32 < seg ? __ldg(wts + K0 + 32 + lane) : 0.f;
-    auto off_of = [&](int e) { return __shfl_sync(0xffffffffu, e < 32 ? offA : offB, e & 31); };
-    auto w_of = [&](int e) { return __shfl_sync(0xffffffffu, e < 32 ? wA : wB, e & 31); };
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq)
-#pragma unroll
-      for (int u = 0; u < kFast; ++u) {
-        const int off = off_of(k0[qq] - K0 + u);  // unconditional: no branch around the shuffle
-        if (u < deg[qq]) {
-          ld(off, v[qq][u]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < V; ++c) v[qq][u][c] = 0.f;
-        }
-      }
-    sparse_noise<V>(a, q, r, z);  // overlaps the gathers' latency
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      float s2[V];
-#pragma unroll
-      for (int c = 0; c < V; ++c) s2[c] = 0.f;
-#pragma unroll
-      for (int u = 0; u < kFast; ++u) {
-        const float wv = w_of(k0[qq] - K0 + u);
-        if (u < deg[qq])
-#pragma unroll
-          for (int c = 0; c < V; ++c) s2[c] = fmaf(wv, v[qq][u][c], s2[c]);  // CSR order
-      }
-#pragma unroll
-      for (int c = 0; c < V; ++c) acc[qq][c] = s2[c];
-    }
-    int dmax = 0;
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq) dmax = max(dmax, deg[qq]);
-    for (int u = kFast; u < dmax; u += kRounds) {
-      float x[kRounds][8][V], wv[kRounds][8];
-#pragma unroll
-      for (int j = 0; j < kRounds; ++j)
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-          if (u + j < deg[qq]) {  // warp-uniform
-            const int e = k0[qq] - K0 + u + j;
-            ld(off_of(e), x[j][qq]);
-            wv[j][qq] = w_of(e);
-          }
-        }
-#pragma unroll
-      for (int j = 0; j < kRounds; ++j)
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq)
-          if (u + j < deg[qq])
-#pragma unroll
-            for (int c = 0; c < V; ++c) acc[qq][c] = fmaf(wv[j][qq], x[j][qq][c], acc[qq][c]);
-    }  } else if (kStaged96 && seg <= 96 && !kDisableStaged) {
-    // Staged segment (rows longer than kFast, up to 64 entries per group:
-    // G-set-class random graphs of mean degree 2-8): every lane holds two
-    // entries of the segment, offsets pre-multiplied, loaded with ONE coalesced
-    // round trip; each gather then takes its offset and weight by shuffle
-    // instead of a dependent global index load (one L2 round trip per round
-    // instead of two).  Same entries, same per-row CSR order from +0: bitwise
-    // the unstaged path.  Measured (tools/csr_probe.py): +20-25% at mean degree
-    // 5, +12% at degree 2.  Not better: staging in shared memory with broadcast
-    // loads (= unstaged), 3-4 registers per lane for 96-128 entries (local
-    // memory; slower than unstaged).
-    const int offA = lane < seg ? __ldg(idx + K0 + lane) * Rp : 0;
-    const int offB = lane + 32 < seg ? __ldg(idx + K0 + 32 + lane) * Rp : 0;
-    const float wA = lane < seg ? __ldg(wts + K0 + lane) : 0.f;
-    const float wB = lane + 32 < seg ? __ldg(wts + K0 + 32 + lane) : 0.f;
-    const int offC = lane + 64 < seg ? __ldg(idx + K0 + 64 + lane) * Rp : 0;
-    const float wC = lane + 64 < seg ? __ldg(wts + K0 + 64 + lane) : 0.f;
+    // k96: a third register for segments up to 96 entries (its own kernel, so the
+    // nested select does not cost the 64-entry kernel)
+    const int offC = k96 && lane + 64 < seg ? __ldg(idx + K0 + 64 + lane) * Rp : 0;
+    const float wC = k96 && lane + 64 < seg ? __ldg(wts + K0 + 64 + lane) : 0.f;
     auto off_of = [&](int e) {
-      return __shfl_sync(0xffffffffu, e < 32 ? offA : (e < 64 ? offB : offC), e & 31);
+      return __shfl_sync(0xffffffffu, e < 32 ? offA : (!k96 || e < 64 ? offB : offC), e & 31);
     };
     auto w_of = [&](int e) {
-      return __shfl_sync(0xffffffffu, e < 32 ? wA : (e < 64 ? wB : wC), e & 31);
+      return __shfl_sync(0xffffffffu, e < 32 ? wA : (!k96 || e < 64 ? wB : wC), e & 31);
     };
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq)
@@ -705,7 +637,8 @@ int launch_sparse_anneal(nmfa_plan* pl, uint64_t key_base, const float* noise,
   else if (ell_k == 4)
     kern = (void*)sparse_ell_kernel<1, 4>;
   else {
-    kern = v2 ? (void*)sparse_step_kernel<2> : (void*)sparse_step_kernel<1>;
+    kern = v2 ? (p->csr_stage96 ? (void*)sparse_step_kernel<2, true> : (void*)sparse_step_kernel<2>)
+              : (void*)sparse_step_kernel<1>;
     kgrid = grid;
   }
   const long long tot = (long long)p->n * pl->Rp;
