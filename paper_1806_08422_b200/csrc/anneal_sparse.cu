@@ -23,7 +23,7 @@
 #define NMFA_CSR_ROUNDS 2
 #endif
 #ifndef NMFA_CSR_ROUNDS_LONG
-#define NMFA_CSR_ROUNDS_LONG 2  // A/B knob: 3 gave +10% at degree 10 but -7% on the staged path
+#define NMFA_CSR_ROUNDS_LONG 2  // the default instances; 3 in the long-segment instance
 #endif
 #ifndef NMFA_FULL_GROUP_STORES
 #define NMFA_FULL_GROUP_STORES 1  // unpredicated state stores for interior groups (+1%)
@@ -193,7 +193,7 @@ __device__ __forceinline__ void sparse_update(const SparseStepArgs& a, int q, in
 // halving the per-update address arithmetic and the uniform CSR overhead of
 // the V = 1 layout (the CSR path is issue-bound; profiles/r01/korder_ab.log).
 // Per replica the arithmetic and summation order are the same for any V.
-template <int V, bool k96 = false>
+template <int V, bool k96 = false, int kRL = NMFA_CSR_ROUNDS_LONG>
 __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
     sparse_step_kernel(const SparseStepArgs a) {
   using Vec = typename std::conditional<V == 2, float2, float>::type;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : NMFA_SPARSE_MINB)
   constexpr int kRounds = NMFA_CSR_ROUNDS;  // entries per row gathered per round beyond kFast
   // segments beyond the staged size (mean degree > 8); 3 entries per row per round trip
   // measured +10% at degree 10 but cost the staged path 7% (register allocation), so 2
-  constexpr int kRoundsLong = V == 2 ? NMFA_CSR_ROUNDS_LONG : NMFA_CSR_ROUNDS;  // V = 1 would spill
+  constexpr int kRoundsLong = V == 2 ? kRL : NMFA_CSR_ROUNDS;  // V = 1 would spill
   const int i_base = 8 * q;
   const int pl = lane <= 8 ? __ldg(a.ptr + min(i_base + lane, n)) : 0;
   int k0[8], deg[8];
@@ -637,8 +637,14 @@ int launch_sparse_anneal(nmfa_plan* pl, uint64_t key_base, const float* noise,
   else if (ell_k == 4)
     kern = (void*)sparse_ell_kernel<1, 4>;
   else {
-    kern = v2 ? (p->csr_stage96 ? (void*)sparse_step_kernel<2, true> : (void*)sparse_step_kernel<2>)
-              : (void*)sparse_step_kernel<1>;
+    // kernel instance by the graph's segment sizes (capi.cu csr_variant): 64-entry staging;
+    // 96-entry staging; 96-entry staging + 3 entries per row per round for longer segments
+    static const char* cv_env = getenv("NMFA_CSR_VARIANT");  // A/B override
+    const int cv = cv_env ? atoi(cv_env) : p->csr_variant;
+    kern = !v2      ? (void*)sparse_step_kernel<1>
+           : cv == 2 ? (void*)sparse_step_kernel<2, true, 3>
+           : cv == 1 ? (void*)sparse_step_kernel<2, true>
+                     : (void*)sparse_step_kernel<2>;
     kgrid = grid;
   }
   const long long tot = (long long)p->n * pl->Rp;

@@ -268,14 +268,16 @@ int nmfa_problem_create(int64_t n, int64_t n_edges, const int64_t* ei_in, const 
     {
       // CSR kernel variant by segment size per 8-spin group (anneal_sparse.cu):
       // the 3-register staged kernel when more groups need 65-96 entries than
-      // fit the 2-register one (33-64): measured +18% at degree 10, -5..9% at 5
-      int64_t mid = 0, big = 0;
+      // fit the 2-register one (33-64): measured +18% at degree 10, -5..9% at 5;
+      // mostly longer segments: also 3 entries per row per round
+      int64_t mid = 0, big = 0, huge = 0;
       for (int64_t g = 0; g * 8 < n; ++g) {
         const int64_t seg = ptr[std::min(n, g * 8 + 8)] - ptr[g * 8];
         mid += seg > 32 && seg <= 64;
         big += seg > 64 && seg <= 96;
+        huge += seg > 96;
       }
-      p->csr_stage96 = big > mid;
+      p->csr_variant = huge > std::max(mid, big) ? 2 : big > mid ? 1 : 0;
     }
     {
       // ELL copy of the CSR rows for low-degree graphs (anneal_sparse.cu). A

@@ -73,9 +73,11 @@ struct nmfa_problem {
   // the same rows as ELL (max degree <= 4): ell_k slots per spin, rows padded
   // to a multiple of 8 spins, short rows padded with (own index, weight 0)
   int32_t ell_k = 0;
-  // CSR kernel variant: segments of 8-spin groups mostly 65-96 entries (mean
-  // degree ~8-12) run the 3-register staged kernel (anneal_sparse.cu)
-  bool csr_stage96 = false;
+  // CSR kernel instance by the segment sizes of the 8-spin groups
+  // (anneal_sparse.cu): 0 = up to 64 entries staged; 1 = mostly 65-96 (3
+  // staged registers); 2 = mostly longer (3 registers + 3 entries per row per
+  // round beyond the staged size)
+  int32_t csr_variant = 0;
   int32_t* d_ell_idx = nullptr;
   float* d_ell_w = nullptr;
   // canonical upper edge list for the exact energy (problem.py:150-154)

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 import paper_1806_08422_b200 as nb  # noqa: E402
 
 HBM = 6545e9
-for n, d in [(5000, 5), (7000, 5), (10000, 2), (10000, 5), (16384, 10)]:
+for n, d in [(5000, 5), (7000, 5), (10000, 2), (10000, 5), (16384, 10), (16384, 16), (16384, 20)]:
     p = nb.gen_dense_maxcut(n, d / (n - 1), 1)
     info = p.device_info()
     for R in (1024, 4096):
