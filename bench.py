@@ -268,11 +268,12 @@ def measure_tts_sk100(nb, dev, skip_cpu=False):
     plan.run(12345, 0, config=cfg, energy=en, stream=stream)       # warm
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     reps = 3
-    ev[0].record(stream)
-    for k in range(reps):
-        plan.run(params.seed + k * R, 0, config=cfg, energy=en, stream=stream)
-    ev[1].record(stream)
-    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:  # the state the K2000 steps left the GPU in is recorded
+        ev[0].record(stream)
+        for k in range(reps):
+            plan.run(params.seed + k * R, 0, config=cfg, energy=en, stream=stream)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
     wall = ev[0].elapsed_time(ev[1]) * 1e-3 / reps
     e = en.cpu().numpy()
     k = int(np.count_nonzero(e <= e_ref + 1e-9))
@@ -280,7 +281,8 @@ def measure_tts_sk100(nb, dev, skip_cpu=False):
     tau = wall / R
     out = {"instance": "gen_sk(100,0), t_f=1000, E_ref=-730 (best of 65,536 reference runs)",
            "gpu": {"reads": R, "p": pg, "tau_s": tau,
-                   "tts99_s": tau * math.log(0.01) / math.log(1 - pg) if 0 < pg < 0.99 else None}}
+                   "tts99_s": tau * math.log(0.01) / math.log(1 - pg) if 0 < pg < 0.99 else None,
+                   "clocks": clk.summary()}}
     try:
         golden = np.load(REF_STATS)
         pref = float(np.mean(golden["sk100_E"] <= e_ref + 1e-9))
