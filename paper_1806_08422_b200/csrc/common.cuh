@@ -147,6 +147,11 @@ __device__ __forceinline__ void box_muller(uint32_t w, float lgs, float& z0, flo
   } else {
     sincos_angle(w & 0xFFFu, sn, cs);
   }
+  // NOTE: a kernel instance in which this product feeds the update's add
+  // directly (seeded-only instances) may have it contracted into an FFMA, one
+  // that merges it with injected noise first may not; instances that must agree
+  // bit for bit (ELL == CSR) therefore share the run-time noise branch
+  // (measured: a seeded-only ELL instance changed the configuration hash).
   z0 = r * cs;
   z1 = r * sn;
 }
