@@ -94,3 +94,22 @@ def test_problem_info_struct_matches_header(tmp_path):
     want = [ctypes.sizeof(_native.ProblemInfo)] + [getattr(_native.ProblemInfo, f).offset
                                                    for f in fields]
     assert got == want, (got, want)
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: without the CUDA library every entry point raises
+    (a fresh interpreter pointed at a missing library file)."""
+    import subprocess
+    import sys
+    prog = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1806_08422_b200._native as N\n"
+        "N.LIB_PATH = '/nonexistent/libnmfa_b200.so'; N._lib = None\n"
+        "import paper_1806_08422_b200 as nb\n"
+        "try:\n"
+        "    nb.nmfa_batch(nb.gen_sk(20, 1), nb.NmfaParams(t_f=10), 4)\n"
+        "except ImportError as e:\n"
+        "    print('RAISED', 'no CPU fallback' in str(e))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", prog], capture_output=True, text=True, timeout=300)
+    assert "RAISED True" in out.stdout, out.stdout + out.stderr[-1500:]
