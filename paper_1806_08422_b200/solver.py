@@ -475,7 +475,17 @@ def _results(problem, res, params, record_trajectory):
 
 
 NOISE_MODES = ("device", "reference")
-REPLAY_CHUNK_BYTES = 1 << 30   # device noise buffer per replay chunk (float32)
+REPLAY_CHUNK_BYTES = 16 << 30  # largest device noise buffer per replay chunk (float32)
+
+
+def _replay_chunk_bytes(device):
+    """Noise buffer per replay chunk: up to REPLAY_CHUNK_BYTES and a quarter
+    of the free device memory, at least 1 GiB.  Larger chunks give the
+    warp-per-run generator more runs (warps) in flight."""
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(device)
+    return int(max(1 << 30, min(REPLAY_CHUNK_BYTES, free // 4)))
 
 
 def reference_noise(seed, n_runs, t_f, n, sigma, *, r0=0, device=0):
@@ -498,7 +508,7 @@ def reference_noise(seed, n_runs, t_f, n, sigma, *, r0=0, device=0):
 
 def _replay(problem, params, n_runs, device, record_trajectory, field=None):
     """Seeded anneals on the reference's own noise streams: replica chunks of
-    at most REPLAY_CHUNK_BYTES of device noise, each generated on the GPU and
+    at most _replay_chunk_bytes() of device noise, each generated on the GPU and
     injected through the run_with_noise seam.  One SampleSet for all runs."""
     import torch
 
@@ -506,7 +516,7 @@ def _replay(problem, params, n_runs, device, record_trajectory, field=None):
     field = _replay_field(problem, device, field)
     n, t_f = problem.n, int(params.t_f)
     temps = params.schedule.temperatures(t_f)
-    chunk = max(1, min(n_runs, REPLAY_CHUNK_BYTES // (4 * t_f * n)))
+    chunk = max(1, min(n_runs, _replay_chunk_bytes(device) // (4 * t_f * n)))
     parts, wall = [], 0.0
     for c0 in range(0, n_runs, chunk):
         c = min(chunk, n_runs - c0)

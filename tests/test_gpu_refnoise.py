@@ -18,6 +18,7 @@ reference's nmfa_batch per seed.
   SURVEY 7).
 """
 
+import os
 import numpy as np
 import pytest
 
@@ -73,3 +74,32 @@ def test_replay_matches_reference_nmfa_batch_per_seed(name):
     print(f"\n{name}[{path}]: identical final energy on {same:.2%} of {reads} seeds; "
           f"mean E {e.mean():.2f} vs reference {ref.mean():.2f}")
     assert same >= need, same
+
+
+_SEQ_PROG = r"""
+import hashlib, sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1806_08422_b200 as nb
+h = hashlib.sha1()
+for seed, R, t_f, n, sigma in [(0, 300, 7, 1429, 0.15), (2**64 - 5, 37, 13, 333, 1.0), (12345, 64, 100, 100, 0.3)]:
+    h.update(nb.reference_noise(seed, R, t_f, n, sigma, r0=17).cpu().numpy().tobytes())
+print("HASH", h.hexdigest())
+"""
+
+
+def test_warp_parallel_stream_equals_sequential_walk():
+    """The warp-per-run generator (default; ballots find where each normal of
+    the counter-based stream starts) equals the one-thread-per-run sequential
+    walk (NMFA_REFNOISE_SEQ=1) bit for bit, over 3 x 10^6 draws including
+    every rejection path (wedge and tail) and counts that end mid-window."""
+    import subprocess
+    import sys as _sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for seq in ("0", "1"):
+        env = dict(os.environ, NMFA_REFNOISE_SEQ=seq)
+        r = subprocess.run([_sys.executable, "-c", _SEQ_PROG, root], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append([ln for ln in r.stdout.splitlines() if ln.startswith("HASH")][-1])
+    assert outs[0] == outs[1]
