@@ -559,9 +559,10 @@ def nmfa_batch(problem, params, n_runs, threads=1, record_trajectory=False, devi
     noise="device" (default) draws in-kernel counter-based Philox noise keyed
     by seed + k (statistically equivalent to the reference, not per seed).
     noise="reference" replays each run's own numpy stream noise_stream(seed +
-    k) generated on the GPU, so run k is comparable per
-    seed with the reference's run k -- slower (the streams are sequential and
-    are injected in replica chunks).  field: the dense path's GEMM operand,
+    k) generated on the GPU (one warp per stream), so run
+    k is comparable per seed with the reference's run k; the noise is injected
+    in replica chunks (K2000: 8192 seeds in under a second).  field: the dense
+    path's GEMM operand,
     "fp16" (hi; the default for device noise) or "hilo" (hi + lo; the default
     for the replay mode), see sample()."""
     n_runs = int(n_runs)
