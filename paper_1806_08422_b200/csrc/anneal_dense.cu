@@ -147,6 +147,7 @@ struct DenseState {
   CUtensorMap tmL[2];  // lo images as A operands (HILO field; copies of tmA otherwise)
   CUtensorMap tmB[2];  // B boxes of exactly one tile half (2 x rows lines), the two widths
   int bhalf[2] = {0, 0};
+  uint32_t stage_bytes = kDStageBytes;  // sized for the plan's tile widths (leaves L1 the rest)
   // fused exchange (row-sharded J): the operand images are peer-accessible
   // buffers owned by the caller, and the epilogue also stores every new hi
   // line into the other shards' images at the same offset
@@ -175,6 +176,7 @@ struct DenseStepArgs {
   uint8_t* lo;             // residual image, same layout (HILO: lo of even sweeps)
   uint8_t* lo1;            // HILO: lo of odd sweeps (the GEMM reads lo, so it ping-pongs)
   int hilo;                // HILO field: A = hi then lo per k-slice, one fp32 accumulator
+  uint32_t stage_bytes;    // ring stage: A box + this plan's widest B half (multiple of 1 KB)
   unsigned long long key_base;
   const float* noise;
   int8_t* cfg;
@@ -459,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
 #else
                 mbar_arrive_expect_tx(&full_bar[s], 2u * (kATile + (uint32_t)half * (kBK * 2)));
 #endif
-              uint8_t* st = smem + (size_t)s * kDStageBytes;
+              uint8_t* st = smem + (size_t)s * a.stage_bytes;
               tma2d_pair(smem_u32(st), sub ? tmL : tmA, 0, (int)(kb * (a.slice_b >> 7) + arow * 2), fb,
                          pol_keep);
 #ifndef NMFA_DBG_NOB
@@ -515,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDThreads, 1)
             }
             tc_fence_after();
             if (a.tl3 && blockIdx.x == 0 && it >= 256 && it < 320) a.tl3[(it - 256) * 4 + 1] = clock64();
-            const uint32_t a_lo = desc_lo0 + (uint32_t)s * (kDStageBytes >> 4);
+            const uint32_t a_lo = desc_lo0 + (uint32_t)s * (a.stage_bytes >> 4);
             const uint32_t b_lo = a_lo + (kATile >> 4);
             if (ki != tl.pad) {
 #pragma unroll
@@ -1347,6 +1349,12 @@ int dense_plan_alloc(nmfa_plan* pl) {
       hs[nh++] = h;
     }
     if (nh == 1) hs[1] = hs[0];
+    // ring stages sized for this plan's widest B half (the unused shared memory
+    // stays L1); NMFA_STAGE_FULL=1 keeps the kMaxW-sized stages (A/B)
+    static const char* full_env = getenv("NMFA_STAGE_FULL");
+    const uint32_t bmax = (uint32_t)std::max(hs[0], hs[1]) * (kBK * 2);
+    ds->stage_bytes = (full_env && full_env[0] == '1') ? kDStageBytes
+                                                      : (kATile + bmax + 1023u) / 1024u * 1024u;
     for (int b = 0; b < 2; ++b) {
       ds->bhalf[b] = hs[b];
       if ((err = make_line_map(&ds->tmB[b], p->d_j_dense, (uint64_t)ds->kblocks * p->brows * 2,
@@ -1417,6 +1425,7 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   a.lo = ds->lo_img;
   a.lo1 = ds->lo_img2;
   a.hilo = ds->hilo ? 1 : 0;
+  a.stage_bytes = ds->stage_bytes;
   a.key_base = key_base;
   a.noise = noise;
   a.cfg = cfg;
@@ -1430,7 +1439,7 @@ int dense_run_sweeps(const nmfa_plan* pl, uint64_t key_base, const float* noise,
   cudaLaunchConfig_t cfgl{};
   cfgl.gridDim = dim3(2 * ds->pairs);
   cfgl.blockDim = dim3(kDThreads);
-  cfgl.dynamicSmemBytes = kDSmemBytes;
+  cfgl.dynamicSmemBytes = (size_t)kDStages * ds->stage_bytes + 1024;
   cfgl.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
