@@ -72,9 +72,13 @@ def test_random_instance_matches_oracle(k):
     ref = np.stack([O.anneal(op, np.zeros(n), temps, noise[r], 0.15)[0] for r in range(R)])
     err = np.abs(S - ref)
     info = f"case {k}: n={n} edges={len(i)} R={R} path={path} int={integer} h={h is not None}"
-    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= 2e-3, (info, err.mean(), err.max())
+    # rare large deviations: at most 0.2% of the elements, and never fewer than one
+    # allowed (a 3-spin, 130-replica case has 390 elements; one replica sitting on a
+    # bifurcation is 0.26%: tools/fuzz_extended.py case 717)
+    rare = max(2e-3, 1.5 / err.size)
+    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= rare, (info, err.mean(), err.max())
     firm = np.abs(ref) > 2e-2
-    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= 2e-3, info
+    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= rare, info
     cfg = O.sign_round(S)
     got, want = nb.energies(p, cfg), O.energies(op, cfg)
     if integer:
@@ -141,9 +145,13 @@ def test_random_large_instance_matches_oracle(k):
     ref = O.batched_anneal(op, None, t_f=t_f, temps=temps, noise=noise)
     err = np.abs(S - ref)
     info = f"case {k}: n={n} edges={len(i)} R={R} path={path} int={integer}"
-    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= 2e-3, (info, err.mean(), err.max())
+    # rare large deviations: at most 0.2% of the elements, and never fewer than one
+    # allowed (a 3-spin, 130-replica case has 390 elements; one replica sitting on a
+    # bifurcation is 0.26%: tools/fuzz_extended.py case 717)
+    rare = max(2e-3, 1.5 / err.size)
+    assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= rare, (info, err.mean(), err.max())
     firm = np.abs(ref) > 2e-2
-    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= 2e-3, info
+    assert np.mean(np.sign(S[firm]) != np.sign(ref[firm])) <= rare, info
     cfg = O.sign_round(S)
     got, want = nb.energies(p, cfg), O.energies(op, cfg)
     if integer:
@@ -178,7 +186,8 @@ def test_random_instance_hilo_field(k):
     if exact:
         assert err.mean() < 1e-5 and err.max() < 1e-3, (info, err.mean(), err.max())
     else:
-        assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= 2e-3, (info, err.mean(), err.max())
+        rare = max(2e-3, 1.5 / err.size)
+        assert err.mean() < 1e-3 and np.mean(err > 2e-2) <= rare, (info, err.mean(), err.max())
     cfg = O.sign_round(S)
     if integer:
         assert np.array_equal(nb.energies(p, cfg), O.energies(op, cfg)), info
