@@ -8,7 +8,12 @@
 // coalesced load.  The group matches the Philox counter granularity, so one
 // Philox call per replica feeds its eight spins (common.cuh noise identity).
 // Both kernels sum each row in CSR order from +0, so they agree bit for bit.
-// Measured design steps: profiles/r01/ell_notes.log, DESIGN.md section 6.
+// The CSR kernel stages a group's segment (<= 64 or <= 96 entries) in lane
+// registers and broadcasts offsets by shuffle; its three instances (64-entry
+// staging, 96-entry staging, 96 + 3 entries per row per round beyond) are
+// chosen per problem from the segment-size histogram (capi.cu csr_variant).
+// Measured design steps: profiles/r01/ell_notes.log, profiles/r02/
+// csr_staged_segments.log, DESIGN.md section 6.
 // Reference: _kernels_numba.py:48-56 (row accumulate, then tanh/mix).
 #include <algorithm>
 #include <cstdio>
