@@ -773,6 +773,30 @@ def run_ours(args):
                          "return type: float64 configs, one dataclass per run; solver.py:262-280)"}
         del runs
 
+    # the dense path's fidelity mode on the same workload (side measurement, K2000 line
+    # only): HILO field, 3 anneals, CUDA events; the algorithmic FLOP as in `roofline`
+    hilo_side = None
+    if (rank == 0 and args.workload == "k2000" and args.field == "fp16" and not args.no_stats
+            and p.device_info(local)["path"] == "dense"):
+        q = build_problem(nb, args.workload)
+        q.device_handle(local).set_field_precision("hilo")
+        hplan = nb.Plan(q, R, temps, params.alpha, params.sigma, device=local)
+        hplan.run(1, r0, config=cfg, energy=en, stream=stream)
+        hev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        hev[0].record(stream)
+        for k in range(3):
+            hplan.run(2 + k, r0, config=cfg, energy=en, stream=stream)
+        hev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        hs = hev[0].elapsed_time(hev[1]) * 1e-3 / 3
+        hilo_side = {"value": n * R * t_f / hs, "unit": "spin-updates/s",
+                     "frac_of_sustained_algorithmic": 2.0 * n * n * R * t_f / hs / 1e12 / peak
+                     if info["path"] == "dense" else None,
+                     "note": "HILO field (hi + lo state through the GEMM, NMFA_FIELD_HILO): the "
+                             "fidelity mode; two MMAs per k-slice, so the executed tensor work is 2x "
+                             "the algorithmic FLOP"}
+        del hplan
+
     tts = None
     if rank == 0 and not args.no_tts:
         tts = measure_tts_sk100(nb, dev, args.no_cpu_baseline)
@@ -814,6 +838,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "tts99_sk100": tts,
             "statistics": stats,
+            **({"hilo_field": hilo_side} if hilo_side else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
