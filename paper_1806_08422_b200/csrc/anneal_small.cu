@@ -213,10 +213,13 @@ __global__ void __launch_bounds__(512, NMFA_SMALL_MINB) small_anneal_kernel(cons
 constexpr size_t kTabBytes = 4096 * sizeof(float2);
 // the sincos table is used when it fits beside J and the operand image(s), at
 // two CTAs per SM while the image alone allowed two (NMFA_SMALL_TABLE=0: never)
-static bool small_table_fits(size_t smem) {
+static bool small_table_fits(size_t smem, int device) {
   static const char* env = getenv("NMFA_SMALL_TABLE");
   if (env && env[0] == '0') return false;
-  const size_t per_sm = 228 * 1024, per_cta = 227 * 1024;
+  int sm_bytes = 228 * 1024, cta_bytes = 227 * 1024;
+  cudaDeviceGetAttribute(&sm_bytes, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&cta_bytes, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const size_t per_sm = (size_t)sm_bytes, per_cta = (size_t)cta_bytes;
   const int ctas_before = (int)std::min<size_t>(2, per_sm / (smem + 1024));
   const int ctas_after = (int)std::min<size_t>(2, per_sm / (smem + kTabBytes + 1024));
   return smem + kTabBytes <= per_cta && ctas_after >= ctas_before;
@@ -261,7 +264,7 @@ int launch_small_anneal(const nmfa_plan* pl, uint64_t key_base, const float* noi
   if (const char* e = getenv("NMFA_SMALL_CS")) a.cs = atoi(e);  // tuning override
   if (a.cs > p->np / 16) a.cs = p->np / 16;
   size_t smem = (size_t)p->np * p->np * 2 + (size_t)kRowsPerCta * p->np * 2 * (1 + a.hilo) + 16;
-  const bool tab = !noise && small_table_fits(smem);
+  const bool tab = !noise && small_table_fits(smem, p->device);
   if (tab) smem += kTabBytes;
   auto kern = noise ? small_anneal_kernel<true, false>
                     : (tab ? small_anneal_kernel<false, true> : small_anneal_kernel<false, false>);
@@ -311,7 +314,7 @@ int launch_small_anneal_many(const nmfa_problem* const* ps, int count, int64_t R
   a.cs = ctas * count >= sms ? 2 : 4;
   if (a.cs > p0->np / 16) a.cs = p0->np / 16;
   size_t smem = (size_t)p0->np * p0->np * 2 + (size_t)kRowsPerCta * p0->np * 2 * (1 + a.hilo) + 16;
-  const bool tab = small_table_fits(smem);
+  const bool tab = small_table_fits(smem, p0->device);
   if (tab) smem += kTabBytes;
   auto kern = tab ? small_anneal_kernel<false, true> : small_anneal_kernel<false, false>;
   NMFA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
