@@ -81,3 +81,39 @@ def write_gset(problem):
     body = "".join(f"{a + 1} {b + 1} {int(x)}\n"
                    for a, b, x in zip(problem.edges_i, problem.edges_j, weights))
     return f"{problem.n} {problem.num_edges}\n" + body
+
+
+# one row per run, fixed column order (reference gset.py:107-130: the results
+# file of the CLI's solve/bench commands)
+RESULT_COLUMNS = ("instance_id", "seed", "final_energy", "cut_value", "wall_clock_us")
+
+
+def write_results_csv(results, metadata):
+    """CSV text of RunResults: instance_id on every row; cut_value when
+    metadata["problem"] has zero fields; wall_clock_us = round(wall_clock * 1e6)
+    when metadata["timings"] is true, else 0 (reruns of the same seeds then give
+    byte-identical files).  Floats are written with repr, like the reference.
+    The cut is (W_total - E) / 2 from each run's exact final energy, the
+    identity the reference's own tests pin (test_problem.py:138-145): equal to
+    its edge sum for integer weights, within an ulp for real ones, and O(1)
+    per row instead of a pass over the edges."""
+    import csv
+    import io
+
+    from .problem import as_problem
+
+    meta = dict(metadata)
+    problem = meta.get("problem")
+    if problem is not None:
+        problem = as_problem(problem)
+    with_cut = problem is not None and not np.any(np.asarray(problem.h) != 0.0)
+    timed = bool(meta.get("timings", False))
+    out = io.StringIO()
+    rows = csv.writer(out, lineterminator="\n")
+    rows.writerow(RESULT_COLUMNS)
+    for run in results:
+        rows.writerow([meta.get("instance_id", ""), run.seed, repr(run.final_energy),
+                       repr((problem.w_total - float(run.final_energy)) * 0.5) if with_cut else "",
+                       int(round(run.wall_clock * 1e6)) if timed else 0])
+    return out.getvalue()
+

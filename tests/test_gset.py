@@ -80,3 +80,25 @@ def test_large_n_without_bitset_still_finds_duplicates():
     assert exc.value.line_no == 4 and "duplicate edge (1, 2)" in str(exc.value)
     p = nb.parse_gset("100000 2\n1 2 1\n99999 100000 -1\n")
     assert p.n == 100000 and p.edges_j.tolist() == [1, 99999]
+
+
+def test_write_results_csv_matches_reference_format():
+    """gset.py:107-130: header, instance id on every row, repr floats, cut from
+    zero-field problems, wall_clock_us only with timings (else 0)."""
+    import numpy as np
+
+    import paper_1806_08422_b200 as nb
+    p = nb.moebius_ladder(8)
+    c = np.array([1.0, -1.0] * 4)
+    runs = [nb.RunResult(final_config=c, final_energy=-4.0, seed=7, wall_clock=1.5e-3),
+            nb.RunResult(final_config=-c, final_energy=-4.0, seed=8, wall_clock=2.5e-6)]
+    w_total = float(np.sum(p.edge_weights))
+    cut = repr((w_total + 4.0) * 0.5)
+    got = nb.write_results_csv(runs, {"instance_id": "m8", "problem": p, "timings": True})
+    assert got == ("instance_id,seed,final_energy,cut_value,wall_clock_us\n"
+                   f"m8,7,-4.0,{cut},1500\nm8,8,-4.0,{cut},2\n")
+    got = nb.write_results_csv(runs, {"instance_id": "m8"})
+    assert got.splitlines()[1:] == ["m8,7,-4.0,,0", "m8,8,-4.0,,0"]
+    hp = nb.IsingProblem(8, [(0, 1, 1.0)], h=[1.0] + [0.0] * 7)
+    assert nb.write_results_csv(runs, {"problem": hp}).splitlines()[1] == ",7,-4.0,,0"
+    assert nb.generators.gen_sk is nb.gen_sk and hasattr(nb.kernels, "install")
