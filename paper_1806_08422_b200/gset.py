@@ -13,7 +13,7 @@ import re
 import numpy as np
 
 from . import _native
-from .problem import IsingProblem
+from .problem import IsingProblem, cut_value  # noqa: F401  (cut_value: the reference's gset namespace)
 
 # non-ASCII characters str.splitlines() / str.split() treat as breaks / spaces
 _NON_ASCII_BREAKS = "\x85\u2028\u2029"

@@ -34,6 +34,9 @@ import numpy as np
 
 from .problem import IsingProblem
 
+BACKEND = "b200"      # kernels.py:13-32: the reference reports its backend here
+FORCE_NUMPY = False   # no CPU backend exists in this package
+
 _CACHE_SIZE = 8
 _cache: "OrderedDict[tuple, tuple]" = OrderedDict()
 _lock = threading.Lock()

@@ -28,7 +28,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native
-from .problem import as_problem, energy  # noqa: F401  (re-exported like the reference)
+from .problem import as_problem, energy, sign_round  # noqa: F401  (re-exported like the reference)
 
 MASK64 = (1 << 64) - 1
 RUN_STREAM_TAG = 2                     # solver.py:33 (numpy noise_stream key space)
