@@ -24,3 +24,45 @@ def test_reference_public_names_exist(module):
     mod = importlib.import_module("paper_1806_08422_b200" + ("." + module if module else ""))
     missing = [n for n in REFERENCE_NAMES[module] if not hasattr(mod, n)]
     assert not missing, (module, missing)
+
+
+# parameter names of the reference's module functions, in order: ours accept the
+# same leading parameters (they may add keyword-only or trailing ones)
+REFERENCE_SIGNATURES = {
+    'generators.gen_cubic_maxcut': ['n', 'seed'],
+    'generators.gen_dense_maxcut': ['n', 'p', 'seed'],
+    'generators.gen_sk': ['n', 'seed'],
+    'generators.is_connected': ['problem'],
+    'generators.moebius_ladder': ['n'],
+    'gset.load_gset': ['path'],
+    'gset.parse_gset': ['text'],
+    'gset.write_gset': ['problem'],
+    'gset.write_results_csv': ['results', 'metadata'],
+    'metrics.aggregate': ['per_instance_stats'],
+    'metrics.brute_force_ground': ['problem'],
+    'metrics.instance_stats': ['results', 'ground', 'tau_seconds', 'confidence'],
+    'metrics.median_iqr': ['values'],
+    'metrics.success_probability': ['results', 'ground'],
+    'metrics.time_to_solution': ['p', 'tau_seconds', 'confidence'],
+    'problem.cut_value': ['problem', 'config'],
+    'problem.energy': ['problem', 'config'],
+    'problem.mean_field': ['problem', 's'],
+    'problem.normalizers': ['problem'],
+    'problem.sign_round': ['s'],
+    'solver.nmfa_batch': ['problem', 'params', 'n_runs', 'threads', 'record_trajectory'],
+    'solver.nmfa_run': ['problem', 'params', 'record_trajectory'],
+    'solver.nmfa_step': ['problem', 's', 'T', 'params', 'rng'],
+    'solver.noise_stream': ['seed'],
+    'solver.run_with_noise': ['problem', 'temps', 'noise', 'alpha', 's0', 'record_trajectory'],
+    'solver.schedule_eval': ['schedule', 't', 't_f'],
+}
+
+
+@pytest.mark.parametrize("qualname", sorted(REFERENCE_SIGNATURES))
+def test_reference_signatures_are_accepted(qualname):
+    import inspect
+    module, name = qualname.split(".")
+    fn = getattr(importlib.import_module("paper_1806_08422_b200." + module), name)
+    ours = [p.name for p in inspect.signature(fn).parameters.values()]
+    want = REFERENCE_SIGNATURES[qualname]
+    assert ours[:len(want)] == want, (qualname, want, ours)
